@@ -1,0 +1,160 @@
+/*
+ * stkde.h -- C ABI of the B200 (sm_100a) space-time kernel density library.
+ *
+ * The library computes, for every voxel (X,Y,T) of a Gx x Gy x Gt grid,
+ *
+ *   f(X,Y,T) = 1/(n hs^2 ht) * sum_{i : sqrt((x-x_i)^2+(y-y_i)^2) < hs and |t-t_i| <= ht}
+ *                  k_s(|x-x_i|/hs, |y-y_i|/hs) * k_t(|t-t_i|/ht)
+ *
+ * with (x,y,t) the voxel centre (x0 + (X+0.5) sres, ...), i.e. the density
+ * of PAPER.md:120-121 (§2.1) with the kernels of PAPER.md:132-133 and the
+ * gates of Alg. 1, accumulated point-major as PB-SYM
+ * (Alg. 3): each point contributes the separable product
+ * K_s(X,Y) * K_t(T) to every voxel of its cylinder.  The GPU computes the
+ * same sum in gather form per voxel tile.
+ *
+ * Conventions for every call:
+ *   - Pointers named d_* are DEVICE pointers on the plan's device; h_* are
+ *     host pointers.  The caller owns all buffers; the plan owns only its
+ *     internal workspace.
+ *   - Points are float32 [n][3] = (x, y, t) in world units, row-major,
+ *     read-only.  Non-finite coordinates are skipped and raise the plan's
+ *     error flag (read with stkde_plan_check).
+ *   - The density grid is float32 [Gx][Gy][Gt], linear index
+ *     (X*Gy + Y)*Gt + T (T innermost; SPEC.md:48-54 layout, 4 B/voxel as in
+ *     the paper's Table 2).  It is FULLY OVERWRITTEN (no
+ *     need to zero it; there is no separate initialisation pass).
+ *   - Calls that take a cudaStream_t (passed as void*) are asynchronous on
+ *     that stream and never synchronise the host; they are CUDA-graph
+ *     capturable.  Their return code reports validation / enqueue errors
+ *     only; kernel faults surface at the caller's next synchronisation.
+ *   - A plan must not be used concurrently from two streams.
+ *   - Results are deterministic: identical inputs give bitwise identical
+ *     grids, and a time slab computed by stkde_compute_slab with a slab
+ *     boundary that is a multiple of the plan's tile height Bt is bitwise
+ *     equal to the same layers of the full-grid result.
+ *   - Return codes: STKDE_OK (0) or a negative STKDE_E* value; the message
+ *     of the most recent error on the calling thread is stkde_last_error().
+ */
+#ifndef STKDE_H_
+#define STKDE_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    STKDE_OK = 0,
+    STKDE_EINVAL = -1,      /* invalid argument (message names the field)            */
+    STKDE_ENOMEM = -2,      /* device allocation failed                              */
+    STKDE_ECUDA = -3,       /* a CUDA runtime call failed                            */
+    STKDE_ECAPACITY = -4,   /* n exceeds the plan's max_n                            */
+    STKDE_ENONFINITE = -5   /* some input coordinate was NaN/Inf (stkde_plan_check)  */
+};
+
+/* Kernel pair (reading R1 in DESIGN.md). */
+enum {
+    STKDE_KERNEL_PRINTED = 0,   /* k_s = pi/2 (1-u)^2 (1-v)^2, k_t = 3/4 (1-w)^2 */
+    STKDE_KERNEL_CLASSICAL = 1  /* k_s = 2/pi (1-u^2-v^2),     k_t = 3/4 (1-w^2)                    */
+};
+
+typedef struct stkde_plan_s *stkde_plan_t;
+
+/* Create a plan on `device` (CUDA ordinal).  Grid origin (x0,y0,t0), voxel
+ * sizes sres/tres > 0, grid Gx,Gy,Gt >= 1 and bandwidths hs, ht > 0 are in
+ * world units (H_s = ceil(hs/sres), H_t = ceil(ht/tres)).
+ * `max_n` bounds the point count of later calls and sizes the device
+ * workspace, so compute calls never allocate.  The tile height Bt is chosen
+ * from H_t (16, 32 or 64); read it back with stkde_plan_info.  Writes the
+ * plan to *out.  Errors: STKDE_EINVAL (message names the field),
+ * STKDE_ENOMEM, STKDE_ECUDA. */
+int stkde_plan_create(stkde_plan_t *out, int device,
+                      double x0, double y0, double t0,
+                      double sres, double tres,
+                      int64_t Gx, int64_t Gy, int64_t Gt,
+                      double hs, double ht,
+                      int kernel_kind, int64_t max_n);
+
+/* Release the plan and its workspace (NULL is a no-op). */
+void stkde_plan_destroy(stkde_plan_t plan);
+
+/* Full grid: d_points [n][3] -> d_grid [Gx][Gy][Gt].  Normalisation
+ * 1/(n hs^2 ht) uses this n; n = 0 writes zeros. */
+int stkde_compute(stkde_plan_t plan, const float *d_points, int64_t n,
+                  float *d_grid, void *stream);
+
+/* Time slab [t_begin, t_end) of the grid, 0 <= t_begin < t_end <= Gt:
+ * d_slab is float32 [Gx][Gy][t_end - t_begin] (T innermost).  `n_norm` is
+ * the n of the normalisation (the GLOBAL point count when the caller shards
+ * one grid over several devices); the point set must be the full one --
+ * points whose temporal window misses the slab are culled on the device, so
+ * the halo is implicit.  Used by the multi-GPU time-slab decomposition
+ * (the temporal split of PAPER.md:415-433). */
+int stkde_compute_slab(stkde_plan_t plan, const float *d_points, int64_t n,
+                       int64_t n_norm, int64_t t_begin, int64_t t_end,
+                       float *d_slab, void *stream);
+
+/* Cost-balanced, Bt-aligned time-slab cuts for `nparts` devices.
+ * Synchronous (reads a per-layer cost histogram back to the host).  Writes
+ * h_cuts[0..nparts] with h_cuts[0] = 0 and h_cuts[nparts] = Gt; empty
+ * slabs are never produced while nparts <= ceil(Gt/Bt).  Cost per layer
+ * T = alpha * (Gx*Gy*4 B)/B_hbm + beta * 2*W(T)/P_fp32 where W(T) is the
+ * number of (point, column) pairs whose window contains T. */
+int stkde_slab_partition(stkde_plan_t plan, const float *d_points, int64_t n,
+                         int nparts, int64_t *h_cuts, void *stream);
+
+/* Exact number C of gated (point, voxel) pairs whose voxel lies in layers
+ * [t_begin, t_end) -- the "contributions" of the metric.  Writes one int64
+ * to d_count (device).  Asynchronous. */
+int stkde_count_contributions(stkde_plan_t plan, const float *d_points, int64_t n,
+                              int64_t t_begin, int64_t t_end, int64_t *d_count,
+                              void *stream);
+
+/* Single-process multi-device driver: plans[d] lives on device d's ordinal,
+ * d_points[d] holds the full point set on that device, d_slabs[d] receives
+ * slab [h_cuts[d], h_cuts[d+1]).  If d_full_grid is non-NULL it must be on
+ * plans[root]'s device and receives the whole grid, gathered over peer
+ * memory (NVLink) by a kernel on the root after all slabs finish.
+ * streams[d] are per-device streams.  Asynchronous except for the cut
+ * computation (stkde_slab_partition on plans[0]) when h_cuts[0] < 0. */
+int stkde_compute_sharded(stkde_plan_t *plans, int ndev,
+                          const float *const *d_points, int64_t n,
+                          float *const *d_slabs, int64_t *h_cuts,
+                          int root, float *d_full_grid, void *const *streams);
+
+/* Synchronises the plan's device; returns STKDE_ENONFINITE if any point of
+ * a previous call had a non-finite coordinate (and clears the flag). */
+int stkde_plan_check(stkde_plan_t plan);
+
+/* Plan facts: tile shape, H, workspace bytes, number of kernels the last
+ * compute launched (library kernels, CUB kernels counted separately). */
+typedef struct {
+    int32_t Bx, By, Bt;
+    int32_t Hs, Ht;
+    int64_t ntiles;
+    int64_t workspace_bytes;
+    int32_t last_own_launches;
+    int32_t last_cub_calls;
+    int32_t tile_threads;
+    int32_t tile_ctas_per_sm;
+    int32_t num_sms;
+    int32_t chunk_candidates;
+} stkde_plan_info_t;
+int stkde_plan_info(stkde_plan_t plan, stkde_plan_info_t *info);
+
+/* Time the tile kernel of subsequent compute calls with CUDA events recorded
+ * on the caller's stream; stkde_plan_kernel_ms sums the elapsed ms of all
+ * timed launches since enable (synchronises on the last event). */
+int stkde_plan_enable_kernel_timing(stkde_plan_t plan, int enable);
+int stkde_plan_kernel_ms(stkde_plan_t plan, double *ms_total, int64_t *launches);
+
+/* Human-readable message for a return code / the last error of this thread. */
+const char *stkde_strerror(int code);
+const char *stkde_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STKDE_H_ */

@@ -1,0 +1,421 @@
+// stkde_api.cu -- C ABI (include/stkde.h): plans, workspace, orchestration.
+//
+// A compute call enqueues, on the caller's stream and without any host
+// synchronisation:
+//   K1 prep + bucket histogram -> CUB radix sort (home-tile key, point idx)
+//   -> permute records -> CUB scan (bucket offsets)          [binning, §3.2]
+//   K3a tile candidate counts -> CUB radix sort (LPT order)
+//   -> K3b chunk pack -> CUB scan -> K3c work items         [work list, §3.3]
+//   tile kernel (persistent, gather form, writes every voxel once)  [§3.4]
+// The workspace is sized at plan creation from max_n, so the sequence is
+// CUDA-graph capturable.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "stkde_internal.cuh"
+
+namespace stkde {
+static thread_local char g_err[512] = "";
+void set_error(const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+}
+}  // namespace stkde
+
+using namespace stkde;
+
+#define CK(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            set_error("%s failed: %s", #call, cudaGetErrorString(e_));                    \
+            return STKDE_ECUDA;                                                           \
+        }                                                                                 \
+    } while (0)
+
+static int key_bits_for(int64_t maxkey) {
+    int b = 1;
+    while (b < 32 && (int64_t(1) << b) <= maxkey) ++b;
+    return b;
+}
+
+static int env_int(const char *name, int dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoi(v) : dflt;
+}
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, double y0, double t0, double sres,
+                                 double tres, int64_t Gx, int64_t Gy, int64_t Gt, double hs, double ht,
+                                 int kernel_kind, int64_t max_n) {
+    if (!out) { set_error("out is NULL"); return STKDE_EINVAL; }
+    *out = nullptr;
+    if (!(sres > 0) || !std::isfinite(sres)) { set_error("sres must be > 0"); return STKDE_EINVAL; }
+    if (!(tres > 0) || !std::isfinite(tres)) { set_error("tres must be > 0"); return STKDE_EINVAL; }
+    if (!(hs > 0) || !std::isfinite(hs)) { set_error("hs must be > 0"); return STKDE_EINVAL; }
+    if (!(ht > 0) || !std::isfinite(ht)) { set_error("ht must be > 0"); return STKDE_EINVAL; }
+    if (!std::isfinite(x0) || !std::isfinite(y0) || !std::isfinite(t0)) { set_error("origin must be finite"); return STKDE_EINVAL; }
+    if (Gx < 1 || Gx > (1 << 22)) { set_error("Gx must be in [1, 2^22]"); return STKDE_EINVAL; }
+    if (Gy < 1 || Gy > (1 << 22)) { set_error("Gy must be in [1, 2^22]"); return STKDE_EINVAL; }
+    if (Gt < 1 || Gt > (1 << 22)) { set_error("Gt must be in [1, 2^22]"); return STKDE_EINVAL; }
+    if (kernel_kind != STKDE_KERNEL_PRINTED && kernel_kind != STKDE_KERNEL_CLASSICAL) { set_error("kernel_kind must be 0 or 1"); return STKDE_EINVAL; }
+    if (max_n < 0 || max_n > ((int64_t)1 << 31) - 1) { set_error("max_n must be in [0, 2^31-1]"); return STKDE_EINVAL; }
+    const double Hs_d = std::ceil(hs / sres), Ht_d = std::ceil(ht / tres);
+    if (Hs_d > 4096 || Ht_d > 4096) { set_error("hs/sres and ht/tres must be <= 4096 voxels"); return STKDE_EINVAL; }
+
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) { set_error("device %d out of range (%d devices)", device, ndev); return STKDE_EINVAL; }
+    CK(cudaSetDevice(device));
+
+    stkde_plan_s *p = (stkde_plan_s *)calloc(1, sizeof(stkde_plan_s));
+    if (!p) { set_error("host allocation failed"); return STKDE_ENOMEM; }
+    p->device = device;
+    CK(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, device));
+    GridParams &g = p->g;
+    g.x0 = x0; g.y0 = y0; g.t0 = t0; g.sres = sres; g.tres = tres; g.hs = hs; g.ht = ht;
+    g.rs = (float)(hs / sres);
+    g.rt = (float)(ht / tres);
+    g.rs2 = (float)((hs / sres) * (hs / sres));
+    g.inv_rs = (float)(sres / hs);
+    g.inv_rt = (float)(tres / ht);
+    g.Gx = (int)Gx; g.Gy = (int)Gy; g.Gt = (int)Gt;
+    g.Hs = (int)Hs_d; g.Ht = (int)Ht_d;
+    // Tile height from the temporal window 2H_t+1.
+    int BT = g.Ht >= 16 ? 64 : (g.Ht >= 6 ? 32 : 16);
+    BT = env_int("STKDE_BT", BT);
+    int C = BT >= 64 ? 1 : 2;
+    C = env_int("STKDE_C", C);
+    if (tile_smem_bytes(BT, C) == 0) { set_error("unsupported tile shape Bt=%d C=%d", BT, C); free(p); return STKDE_EINVAL; }
+    g.BT = BT;
+    p->C = C;
+    p->kernel = kernel_kind;
+    g.kernel = kernel_kind;
+    p->tile_threads = 256 / C;
+    g.NTX = (int)((Gx + BX - 1) / BX);
+    g.NTY = (int)((Gy + BY - 1) / BY);
+    g.NTT = (int)((Gt + BT - 1) / BT);
+    g.Ra = (g.Hs + BX - 1) / BX;
+    g.Rt = (g.Ht + BT - 1) / BT;
+    p->ntiles = (int64_t)g.NTX * g.NTY * g.NTT;
+    if (p->ntiles >= ((int64_t)1 << 30)) { set_error("grid has too many tiles"); free(p); return STKDE_EINVAL; }
+    const int64_t nseg_max = (int64_t)std::min(2 * g.Ra + 1, g.NTY) * std::min(2 * g.Rt + 1, g.NTT);
+    if (nseg_max > MAXSEG) { set_error("bandwidth too large for the tile shape (%lld segments)", (long long)nseg_max); free(p); return STKDE_EINVAL; }
+    p->max_n = max_n;
+    p->key_bits = key_bits_for(p->ntiles);
+
+    // Work-item and split-slot bounds: total candidates <= n * buckets per tile.
+    const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ra + 1, g.NTY) *
+                       std::min(2 * g.Rt + 1, g.NTT);
+    const int64_t cand_bound = std::max<int64_t>(max_n, 1) * nb;
+    const size_t tile_bytes = (size_t)256 * BT * 4;
+    const int64_t slot_budget = (int64_t)env_int("STKDE_SLOT_MB", 1024) * (1 << 20) / (int64_t)tile_bytes;
+    int64_t chunk = std::max<int64_t>(env_int("STKDE_CHUNK", 4096), (2 * cand_bound + slot_budget - 1) / slot_budget);
+    chunk = std::min<int64_t>(chunk, (int64_t)1 << 30);
+    p->chunk = (int)chunk;
+    p->max_items = p->ntiles + cand_bound / chunk + 1;
+    p->max_slots = 2 * (cand_bound / chunk) + 2;
+    p->smem_bytes = tile_smem_bytes(BT, C);
+    int rc = tile_occupancy(BT, C, kernel_kind, &p->ctas_per_sm);
+    if (rc != STKDE_OK) { set_error("tile kernel attribute/occupancy query failed"); free(p); return rc; }
+    if (p->ctas_per_sm < 1) { set_error("tile kernel does not fit on an SM"); free(p); return STKDE_EINVAL; }
+
+    // CUB temporary storage: max over the four calls at their largest sizes.
+    const int nmax = (int)std::max<int64_t>(max_n, 1);
+    size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                       (uint32_t *)nullptr, nmax, 0, p->key_bits));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)(p->ntiles + 1)));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, b3, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
+                                       (uint32_t *)nullptr, (int)p->ntiles, 0, 32));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b4, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)(p->ntiles + 1)));
+    p->cub_bytes = std::max(std::max(b1, b2), std::max(b3, b4));
+
+    // One workspace allocation, carved.
+    struct Part { void **ptr; size_t bytes; };
+    const size_t nrec = (size_t)std::max<int64_t>(max_n, 1);
+    const size_t nt = (size_t)p->ntiles;
+    Part parts[] = {
+        {(void **)&p->rec, nrec * sizeof(PointRec)},
+        {(void **)&p->rec_sorted, nrec * sizeof(PointRec)},
+        {(void **)&p->keys_in, nrec * 4}, {(void **)&p->keys_out, nrec * 4},
+        {(void **)&p->vals_in, nrec * 4}, {(void **)&p->vals_out, nrec * 4},
+        {(void **)&p->bucket_cnt, (nt + 1) * 4}, {(void **)&p->bucket_begin, (nt + 2) * 4},
+        {(void **)&p->lpt_key_in, nt * 4}, {(void **)&p->lpt_key_out, nt * 4},
+        {(void **)&p->lpt_val_in, nt * 4}, {(void **)&p->lpt_val_out, nt * 4},
+        {(void **)&p->chunk_pack, (nt + 1) * 8}, {(void **)&p->chunk_off, (nt + 1) * 8},
+        {(void **)&p->items, (size_t)p->max_items * 16},
+        {(void **)&p->arrive, nt * 4},
+        {(void **)&p->partials, (size_t)p->max_slots * tile_bytes},
+        {(void **)&p->counters, 64 * 4},
+        {(void **)&p->hist_t, ((size_t)Gt + 1) * 4},
+        {(void **)&p->cub_tmp, p->cub_bytes},
+    };
+    size_t total = 0;
+    for (auto &pt : parts) total = align_up(total, 256) + pt.bytes;
+    cudaError_t e = cudaMalloc(&p->ws, total);
+    if (e != cudaSuccess) {
+        set_error("workspace allocation of %zu bytes failed: %s", total, cudaGetErrorString(e));
+        free(p);
+        return STKDE_ENOMEM;
+    }
+    p->ws_bytes = total;
+    size_t off = 0;
+    for (auto &pt : parts) {
+        off = align_up(off, 256);
+        *pt.ptr = (char *)p->ws + off;
+        off += pt.bytes;
+    }
+    CK(cudaMemset(p->arrive, 0, nt * 4));
+    CK(cudaMemset(p->counters, 0, 64 * 4));
+    *out = p;
+    return STKDE_OK;
+}
+
+extern "C" void stkde_plan_destroy(stkde_plan_t p) {
+    if (!p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(p->device);
+    cudaFree(p->ws);
+    for (int i = 0; i < 2 * p->tev_cap; ++i) cudaEventDestroy(p->tev[i]);
+    free(p->tev);
+    cudaSetDevice(cur);
+    free(p);
+}
+
+// Sum the recorded tile-kernel intervals (synchronises on the last stop event).
+static void harvest_timing(stkde_plan_s *p) {
+    for (int i = 0; i < p->tev_used; ++i) {
+        float ms = 0.f;
+        if (cudaEventSynchronize(p->tev[2 * i + 1]) == cudaSuccess &&
+            cudaEventElapsedTime(&ms, p->tev[2 * i], p->tev[2 * i + 1]) == cudaSuccess) {
+            p->kernel_ms += ms;
+            p->kernel_launches += 1;
+        }
+    }
+    p->tev_used = 0;
+}
+
+static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, int64_t n_norm, int64_t t_begin,
+                             int64_t t_end, float *d_out, cudaStream_t st) {
+    const GridParams &g = p->g;
+    p->last_own_launches = 0;
+    p->last_cub_calls = 0;
+    if (n < 0 || n_norm < 0) { set_error("n must be >= 0"); return STKDE_EINVAL; }
+    if (n > p->max_n) { set_error("n = %lld exceeds the plan's max_n = %lld", (long long)n, (long long)p->max_n); return STKDE_ECAPACITY; }
+    if (t_begin < 0 || t_end > g.Gt || t_begin >= t_end) { set_error("slab [t_begin, t_end) must satisfy 0 <= t_begin < t_end <= Gt"); return STKDE_EINVAL; }
+    if (!d_out || (n > 0 && !d_points)) { set_error("NULL device pointer"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    const int64_t Ts = t_end - t_begin;
+    if (n == 0 || n_norm == 0) {   // empty point set -> zeros, no division
+        CK(cudaMemsetAsync(d_out, 0, (size_t)g.Gx * g.Gy * Ts * sizeof(float), st));
+        return STKDE_OK;
+    }
+    // 1/(n hs^2 ht) times the kernel constant (pi/2 or 2/pi).
+    const double kc = p->kernel == STKDE_KERNEL_PRINTED ? M_PI / 2.0 : 2.0 / M_PI;
+    const float cnorm = (float)(kc / ((double)n_norm * (g.hs * g.hs) * g.ht));
+    int rc = launch_binning(p, d_points, n, st);
+    if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    const int c0 = (int)(t_begin / g.BT), c1 = (int)((t_end + g.BT - 1) / g.BT);
+    rc = launch_worklist(p, c0, c1, st);
+    if (rc) { set_error("work-list launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    rc = launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
+    if (rc) { set_error("tile kernel launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    return STKDE_OK;
+}
+
+extern "C" int stkde_compute(stkde_plan_t p, const float *d_points, int64_t n, float *d_grid, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    return compute_slab_impl(p, d_points, n, n, 0, p->g.Gt, d_grid, (cudaStream_t)stream);
+}
+
+extern "C" int stkde_compute_slab(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm, int64_t t_begin,
+                                  int64_t t_end, float *d_slab, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    return compute_slab_impl(p, d_points, n, n_norm, t_begin, t_end, d_slab, (cudaStream_t)stream);
+}
+
+extern "C" int stkde_count_contributions(stkde_plan_t p, const float *d_points, int64_t n, int64_t t_begin,
+                                         int64_t t_end, int64_t *d_count, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    if (n < 0 || (n > 0 && !d_points) || !d_count) { set_error("bad points/count arguments"); return STKDE_EINVAL; }
+    if (t_begin < 0 || t_end > p->g.Gt || t_begin >= t_end) { set_error("bad slab"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    int rc = launch_count(p, d_points, n, t_begin, t_end, d_count, (cudaStream_t)stream);
+    if (rc) set_error("count launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return rc;
+}
+
+// Cost-balanced Bt-aligned cuts: per-layer cost =
+//   Gx*Gy*4 B / B_hbm  +  2 * W(T) / P_fp32,
+// W(T) = (disc columns) * #{points whose window contains T}.
+extern "C" int stkde_slab_partition(stkde_plan_t p, const float *d_points, int64_t n, int nparts, int64_t *h_cuts,
+                                    void *stream) {
+    if (!p || !h_cuts || nparts < 1) { set_error("bad arguments"); return STKDE_EINVAL; }
+    const GridParams &g = p->g;
+    CK(cudaSetDevice(p->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<int> hist(g.Gt + 1, 0);
+    if (n > 0) {
+        int rc = launch_hist_t(p, d_points, n, st);
+        if (rc) { set_error("histogram launch failed"); return rc; }
+        CK(cudaMemcpyAsync(hist.data(), p->hist_t, g.Gt * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    const double B_hbm = 6.5e12, P_fp32 = 6.0e13;
+    const double disc = M_PI * (double)g.rs * g.rs;
+    std::vector<double> pre(g.Gt + 2, 0.0);   // prefix of point counts by T_i
+    for (int T = 0; T < g.Gt; ++T) pre[T + 1] = pre[T] + hist[T];
+    const int nblk = g.NTT;
+    std::vector<double> cost(nblk, 0.0);
+    for (int T = 0; T < g.Gt; ++T) {
+        int lo = std::max(T - g.Ht, 0), hi = std::min(T + g.Ht, g.Gt - 1);
+        double w = (pre[hi + 1] - pre[lo]) * disc;
+        cost[T / g.BT] += (double)g.Gx * g.Gy * 4.0 / B_hbm + 2.0 * w / P_fp32;
+    }
+    double tot = 0;
+    for (double c : cost) tot += c;
+    h_cuts[0] = 0;
+    int b = 0;
+    double acc = 0;
+    for (int k = 1; k < nparts; ++k) {
+        const double target = tot * k / nparts;
+        const int min_b = (int)h_cuts[k - 1] / g.BT + 1;          // at least one tile layer per part
+        const int max_b = nblk - (nparts - k);                      // leave one per remaining part
+        while (b < nblk && (acc + cost[b] * 0.5 < target || b < min_b)) { acc += cost[b]; ++b; }
+        int bb = std::min(std::max(b, min_b), std::max(max_b, min_b));
+        while (b < bb) { acc += cost[b]; ++b; }
+        h_cuts[k] = std::min<int64_t>((int64_t)bb * g.BT, g.Gt);
+    }
+    h_cuts[nparts] = g.Gt;
+    for (int k = 1; k <= nparts; ++k)
+        if (h_cuts[k] < h_cuts[k - 1]) h_cuts[k] = h_cuts[k - 1];
+    return STKDE_OK;
+}
+
+extern "C" int stkde_compute_sharded(stkde_plan_t *plans, int ndev, const float *const *d_points, int64_t n,
+                                     float *const *d_slabs, int64_t *h_cuts, int root, float *d_full_grid,
+                                     void *const *streams) {
+    if (!plans || ndev < 1 || !d_points || !d_slabs || !h_cuts || !streams) { set_error("bad arguments"); return STKDE_EINVAL; }
+    for (int d = 0; d < ndev; ++d)
+        if (!plans[d]) { set_error("plans[%d] is NULL", d); return STKDE_EINVAL; }
+    if (h_cuts[0] < 0) {
+        int rc = stkde_slab_partition(plans[0], d_points[0], n, ndev, h_cuts, streams[0]);
+        if (rc) return rc;
+    }
+    for (int d = 0; d < ndev; ++d) {
+        if (h_cuts[d + 1] <= h_cuts[d]) continue;   // empty slab
+        int rc = stkde_compute_slab(plans[d], d_points[d], n, n, h_cuts[d], h_cuts[d + 1], d_slabs[d], streams[d]);
+        if (rc) return rc;
+    }
+    if (d_full_grid) {
+        if (root < 0 || root >= ndev) { set_error("root out of range"); return STKDE_EINVAL; }
+        stkde_plan_s *pr = plans[root];
+        CK(cudaSetDevice(pr->device));
+        cudaStream_t rs = (cudaStream_t)streams[root];
+        for (int d = 0; d < ndev; ++d) {
+            if (h_cuts[d + 1] <= h_cuts[d]) continue;
+            if (plans[d]->device != pr->device) {
+                int can = 0;
+                CK(cudaDeviceCanAccessPeer(&can, pr->device, plans[d]->device));
+                if (!can) { set_error("device %d cannot access device %d", pr->device, plans[d]->device); return STKDE_ECUDA; }
+                cudaError_t e = cudaDeviceEnablePeerAccess(plans[d]->device, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                cudaGetLastError();
+                cudaEvent_t ev;
+                CK(cudaSetDevice(plans[d]->device));
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, (cudaStream_t)streams[d]));
+                CK(cudaSetDevice(pr->device));
+                CK(cudaStreamWaitEvent(rs, ev, 0));
+                cudaEventDestroy(ev);
+            } else if (streams[d] != streams[root]) {
+                cudaEvent_t ev;
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, (cudaStream_t)streams[d]));
+                CK(cudaStreamWaitEvent(rs, ev, 0));
+                cudaEventDestroy(ev);
+            }
+            int rc = launch_gather(d_slabs[d], pr->g.Gx, pr->g.Gy, pr->g.Gt, h_cuts[d], h_cuts[d + 1], d_full_grid, rs);
+            if (rc) { set_error("gather launch failed"); return rc; }
+        }
+    }
+    return STKDE_OK;
+}
+
+extern "C" int stkde_plan_check(stkde_plan_t p) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    CK(cudaDeviceSynchronize());
+    int flags = 0;
+    CK(cudaMemcpy(&flags, p->counters + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(p->counters + 1, 0, sizeof(int)));
+    if (flags & 2) { set_error("internal work-list capacity exceeded"); return STKDE_ECUDA; }
+    if (flags & 1) { set_error("non-finite point coordinate(s) were skipped"); return STKDE_ENONFINITE; }
+    return STKDE_OK;
+}
+
+extern "C" int stkde_plan_info(stkde_plan_t p, stkde_plan_info_t *info) {
+    if (!p || !info) { set_error("NULL argument"); return STKDE_EINVAL; }
+    info->Bx = BX; info->By = BY; info->Bt = p->g.BT;
+    info->Hs = p->g.Hs; info->Ht = p->g.Ht;
+    info->ntiles = p->ntiles;
+    info->workspace_bytes = (int64_t)p->ws_bytes;
+    info->last_own_launches = p->last_own_launches;
+    info->last_cub_calls = p->last_cub_calls;
+    info->tile_threads = p->tile_threads;
+    info->tile_ctas_per_sm = p->ctas_per_sm;
+    info->num_sms = p->num_sms;
+    info->chunk_candidates = p->chunk;
+    return STKDE_OK;
+}
+
+extern "C" int stkde_plan_enable_kernel_timing(stkde_plan_t p, int enable) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    if (enable && !p->tev) {
+        const int cap = 4096;
+        p->tev = (cudaEvent_t *)calloc(2 * cap, sizeof(cudaEvent_t));
+        if (!p->tev) { set_error("host allocation failed"); return STKDE_ENOMEM; }
+        for (int i = 0; i < 2 * cap; ++i) CK(cudaEventCreate(&p->tev[i]));
+        p->tev_cap = cap;
+    }
+    p->tev_used = 0;
+    p->timing = enable ? 1 : 0;
+    p->kernel_ms = 0;
+    p->kernel_launches = 0;
+    return STKDE_OK;
+}
+
+extern "C" int stkde_plan_kernel_ms(stkde_plan_t p, double *ms_total, int64_t *launches) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    harvest_timing(p);
+    if (ms_total) *ms_total = p->kernel_ms;
+    if (launches) *launches = p->kernel_launches;
+    return STKDE_OK;
+}
+
+extern "C" const char *stkde_strerror(int code) {
+    switch (code) {
+        case STKDE_OK: return "ok";
+        case STKDE_EINVAL: return "invalid argument";
+        case STKDE_ENOMEM: return "device allocation failed";
+        case STKDE_ECUDA: return "CUDA error";
+        case STKDE_ECAPACITY: return "n exceeds plan capacity (max_n)";
+        case STKDE_ENONFINITE: return "non-finite point coordinate";
+    }
+    return "unknown error";
+}
+
+extern "C" const char *stkde_last_error(void) { return g_err; }

@@ -1,0 +1,187 @@
+// stkde_internal.cuh -- plan layout, kernel parameters and the device-side
+// geometry helpers (voxel mapping, exact gates, per-row disc chords) of the
+// B200 STKDE library.  Nothing here is shared with oracle/.
+//
+// Paper references (PAPER.md = /root/reference/PAPER.md):
+//   density and kernels     PAPER.md:120-133 (§2.1)
+//   gates                   Alg. 1, PAPER.md:208 (spatial strict, temporal inclusive)
+//   grid / H
+//   PB-SYM separability     Alg. 3; Fig. 3
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/stkde.h"
+
+namespace stkde {
+
+constexpr int BX = 16;            // tile width in X (voxels)
+constexpr int BY = 16;            // tile width in Y (voxels)
+constexpr int MAXSEG = 256;       // max home-bucket segments per tile
+// Relative band around the disc edge inside which the FP32 gate defers to
+// the exact FP64 expression (reading R13): |d^2 - r^2| <= BAND r^2.
+constexpr float GATE_BAND = 1e-4f;
+
+// Per-point record written by the prep kernel (32 B, one per input point).
+//   X, Y, T     voxel of the point: floor((x - x0)/sres) ...
+//   fx, fy, ft  fractional position inside that voxel, in voxel units, [0,1)
+//   x, y        the original FP32 world coordinates (for the FP64 gate)
+struct __align__(16) PointRec {
+    int X, Y, T;
+    float fx, fy, ft;
+    float x, y;
+};
+
+// Kernel-side view of a plan (passed by value).
+struct GridParams {
+    double x0, y0, t0;      // origin (world)
+    double sres, tres;      // voxel sizes (world)
+    double hs, ht;          // bandwidths (world)
+    float rs, rt;           // hs/sres, ht/tres (voxel units)
+    float rs2;              // rs*rs
+    float inv_rs, inv_rt;   // sres/hs, tres/ht
+    int Gx, Gy, Gt;         // grid (voxels)
+    int Hs, Ht;             // ceil(hs/sres), ceil(ht/tres)
+    int NTX, NTY, NTT;      // tiles per axis
+    int BT;                 // tile height (layers)
+    int Ra, Rt;             // home-bucket reach in tiles: ceil(Hs/BX), ceil(Ht/BT)
+    int kernel;             // STKDE_KERNEL_*
+};
+
+__host__ __device__ inline int floordiv(int a, int b) {
+    int q = a / b;
+    return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+// ---- exact FP64 gates: the same IEEE expression sequence as Alg. 1 ----
+// x = x0 + (X + 0.5) sres (voxel centre), dx = x - x_i,
+// inside iff sqrt(dx*dx + dy*dy) < hs.  No contraction: __dmul_rn/__dadd_rn.
+__device__ __forceinline__ bool gate_s_fp64(const GridParams &g, int X, int Y, float px, float py) {
+    double cx = __dadd_rn(g.x0, __dmul_rn(__dadd_rn((double)X, 0.5), g.sres));
+    double cy = __dadd_rn(g.y0, __dmul_rn(__dadd_rn((double)Y, 0.5), g.sres));
+    double dx = __dsub_rn(cx, (double)px);
+    double dy = __dsub_rn(cy, (double)py);
+    double d = __dsqrt_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)));
+    return d < g.hs;
+}
+// |t - t_i| <= ht with t = t0 + (T + 0.5) tres.
+__device__ __forceinline__ bool gate_t_fp64(const GridParams &g, int T, float pt) {
+    double ct = __dadd_rn(g.t0, __dmul_rn(__dadd_rn((double)T, 0.5), g.tres));
+    return fabs(__dsub_rn(ct, (double)pt)) <= g.ht;
+}
+
+// Spatial gate of column X in a row whose FP32 offset^2 is dy2 (voxel units):
+// FP32 unless |d^2 - r^2| is within the band, then the exact FP64 gate.
+__device__ __forceinline__ bool gate_s(const GridParams &g, const PointRec &r, int X, int Y, float dy2) {
+    float dxv = (float)(X - r.X) + 0.5f - r.fx;
+    float d2 = __fadd_rn(__fmul_rn(dxv, dxv), dy2);
+    float diff = d2 - g.rs2;
+    if (fabsf(diff) > GATE_BAND * g.rs2) return diff < 0.0f;
+    return gate_s_fp64(g, X, Y, r.x, r.y);
+}
+
+// Exact chord of the disc of point r on row Y: the global column interval
+// [*lo, *hi] whose voxel centres pass the spatial gate (empty: *lo > *hi).
+// The in-set of a row is an interval because the FP64 gate is monotone in
+// |X + 0.5 - p|; the FP32 estimate is within one column of each end and is
+// corrected with the exact gate.
+__device__ __forceinline__ void row_chord(const GridParams &g, const PointRec &r, int Y, int *lo, int *hi) {
+    float dyv = (float)(Y - r.Y) + 0.5f - r.fy;
+    float dy2 = __fmul_rn(dyv, dyv);
+    if (dy2 > g.rs2 * (1.0f + GATE_BAND) || !gate_s(g, r, r.X, Y, dy2)) {
+        *lo = 1; *hi = 0;
+        return;
+    }
+    float c = sqrtf(fmaxf(g.rs2 - dy2, 0.0f));
+    float pc = (float)r.X + r.fx - 0.5f;            // column coordinate of the point
+    int a = (int)floorf(pc - c) + 1, b = (int)ceilf(pc + c) - 1;
+    a = min(a, r.X);
+    b = max(b, r.X);
+    while (a < r.X && !gate_s(g, r, a, Y, dy2)) ++a;
+    while (gate_s(g, r, a - 1, Y, dy2)) --a;
+    while (b > r.X && !gate_s(g, r, b, Y, dy2)) --b;
+    while (gate_s(g, r, b + 1, Y, dy2)) ++b;
+    *lo = a;
+    *hi = b;
+}
+
+// Row mask of the 16 tile columns [tX0, tX0+16) inside the disc on row Y.
+__device__ __forceinline__ uint32_t row_mask16(const GridParams &g, const PointRec &r, int tX0, int Y) {
+    float dyv = (float)(Y - r.Y) + 0.5f - r.fy;
+    float dy2 = __fmul_rn(dyv, dyv);
+    // quick accept / reject from the two tile-edge columns and the nearest column
+    float p = (float)(r.X - tX0) + r.fx - 0.5f;     // point in tile-local column coordinates
+    float e0 = p, e1 = 15.0f - p;                     // distances to the edge columns
+    float far = fmaxf(fabsf(e0), fabsf(e1));
+    if (__fadd_rn(__fmul_rn(far, far), dy2) < g.rs2 * (1.0f - GATE_BAND)) return 0xFFFFu;
+    float nearx = fminf(fmaxf(p, 0.0f), 15.0f) - p;
+    if (__fadd_rn(__fmul_rn(nearx, nearx), dy2) > g.rs2 * (1.0f + GATE_BAND)) return 0u;
+    int lo, hi;
+    row_chord(g, r, Y, &lo, &hi);
+    lo = max(lo - tX0, 0);
+    hi = min(hi - tX0, 15);
+    if (lo > hi) return 0u;
+    return ((2u << hi) - 1u) & ~((1u << lo) - 1u);
+}
+
+}  // namespace stkde
+
+// ------------------------------------------------------------------ plan ---
+struct stkde_plan_s {
+    int device;
+    int num_sms;
+    stkde::GridParams g;
+    int kernel;
+    int C;                    // columns per thread of the tile kernel
+    int tile_threads;
+    int ctas_per_sm;
+    int64_t max_n;
+    int64_t ntiles;           // NTX*NTY*NTT (global)
+    int key_bits;             // radix bits of the home-bucket keys
+    int chunk;                // candidates per work item
+    int64_t max_items;
+    int64_t max_slots;        // split-tile partial slots
+    size_t smem_bytes;
+
+    // workspace
+    void *ws;
+    size_t ws_bytes;
+    stkde::PointRec *rec, *rec_sorted;
+    uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
+    uint32_t *bucket_cnt;       // [ntiles + 1]
+    uint32_t *bucket_begin;     // [ntiles + 2]
+    uint32_t *lpt_key_in, *lpt_key_out, *lpt_val_in, *lpt_val_out;   // [ntiles]
+    uint64_t *chunk_pack, *chunk_off;   // [ntiles + 1]
+    int4 *items;                // [max_items]
+    uint32_t *arrive;           // [ntiles]
+    float *partials;            // [max_slots][256*BT]
+    int *counters;              // [0] work counter, [1] error flag, [2..] spare
+    int *hist_t;                // [Gt + 1] slab-partition histogram
+    void *cub_tmp;
+    size_t cub_bytes;
+
+    // instrumentation
+    int timing;
+    cudaEvent_t *tev;         // [2 * tev_cap] start/stop pairs around tile launches
+    int tev_cap, tev_used;
+    double kernel_ms;
+    int64_t kernel_launches;
+    int last_own_launches, last_cub_calls;
+};
+
+namespace stkde {
+// launchers (stkde_binning.cu / stkde_tile.cu)
+int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
+int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
+int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,
+                float *out, cudaStream_t st);
+int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_begin,
+                 int64_t t_end, int64_t *d_count, cudaStream_t st);
+int launch_hist_t(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
+int launch_gather(const float *slab, int64_t Gx, int64_t Gy, int64_t Gt, int64_t t0, int64_t t1,
+                  float *full, cudaStream_t st);
+size_t tile_smem_bytes(int BT, int C);
+int tile_occupancy(int BT, int C, int kernel, int *ctas_per_sm);
+void set_error(const char *fmt, ...);
+}  // namespace stkde

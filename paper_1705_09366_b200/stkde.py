@@ -1,0 +1,238 @@
+"""Thin ctypes binding over libstkde.so (include/stkde.h).
+
+Argument marshalling only: every step of the density computation runs in the
+CUDA kernels of csrc/.  There is no CPU fallback -- if the library or a CUDA
+device is missing the calls raise.  PyTorch supplies device memory, streams
+and (for the sharded path) process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libstkde.so")
+
+STKDE_OK, STKDE_EINVAL, STKDE_ENOMEM, STKDE_ECUDA, STKDE_ECAPACITY, STKDE_ENONFINITE = 0, -1, -2, -3, -4, -5
+KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
+
+# Exported entry points of include/stkde.h (checked by tests/test_abi.py).
+EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_compute_slab",
+           "stkde_slab_partition", "stkde_count_contributions", "stkde_compute_sharded",
+           "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
+           "stkde_plan_kernel_ms", "stkde_strerror", "stkde_last_error")
+
+
+class StkdeError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__("stkde error %d: %s" % (code, msg))
+        self.code = code
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("Bx", ctypes.c_int32), ("By", ctypes.c_int32), ("Bt", ctypes.c_int32),
+                ("Hs", ctypes.c_int32), ("Ht", ctypes.c_int32),
+                ("ntiles", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+                ("last_own_launches", ctypes.c_int32), ("last_cub_calls", ctypes.c_int32),
+                ("tile_threads", ctypes.c_int32), ("tile_ctas_per_sm", ctypes.c_int32),
+                ("num_sms", ctypes.c_int32), ("chunk_candidates", ctypes.c_int32)]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libstkde.so (raises if it was not built: `python -m paper_1705_09366_b200.build`)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise FileNotFoundError("libstkde.so not built at %s (run python -m paper_1705_09366_b200.build)" % path)
+    L = ctypes.CDLL(path)
+    P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
+    L.stkde_plan_create.argtypes = [ctypes.POINTER(P), I32, D, D, D, D, D, I64, I64, I64, D, D, I32, I64]
+    L.stkde_plan_destroy.argtypes = [P]
+    L.stkde_plan_destroy.restype = None
+    L.stkde_compute.argtypes = [P, P, I64, P, P]
+    L.stkde_compute_slab.argtypes = [P, P, I64, I64, I64, I64, P, P]
+    L.stkde_slab_partition.argtypes = [P, P, I64, I32, ctypes.POINTER(I64), P]
+    L.stkde_count_contributions.argtypes = [P, P, I64, I64, I64, P, P]
+    L.stkde_compute_sharded.argtypes = [ctypes.POINTER(P), I32, ctypes.POINTER(P), I64, ctypes.POINTER(P),
+                                        ctypes.POINTER(I64), I32, P, ctypes.POINTER(P)]
+    L.stkde_plan_check.argtypes = [P]
+    L.stkde_plan_info.argtypes = [P, ctypes.POINTER(PlanInfo)]
+    L.stkde_plan_enable_kernel_timing.argtypes = [P, I32]
+    L.stkde_plan_kernel_ms.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(I64)]
+    L.stkde_strerror.argtypes = [I32]
+    L.stkde_strerror.restype = ctypes.c_char_p
+    L.stkde_last_error.argtypes = []
+    L.stkde_last_error.restype = ctypes.c_char_p
+    for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition",
+                 "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
+                 "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms"):
+        getattr(L, name).restype = I32
+    _lib = L
+    return L
+
+
+def _check(rc: int):
+    if rc != STKDE_OK:
+        L = load_library()
+        raise StkdeError(rc, L.stkde_last_error().decode() or L.stkde_strerror(rc).decode())
+    return rc
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream], device) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    return int(s.cuda_stream)
+
+
+def _points_arg(points: torch.Tensor, device: torch.device) -> torch.Tensor:
+    if not isinstance(points, torch.Tensor) or points.device != device:
+        raise ValueError("points must be a CUDA tensor on %s" % device)
+    if points.dtype != torch.float32 or points.dim() != 2 or points.shape[1] != 3:
+        raise ValueError("points must be float32 [n, 3] (x, y, t)")
+    return points.contiguous()
+
+
+class Plan:
+    """A density plan on one device (stkde_plan_create); owns the device workspace."""
+
+    def __init__(self, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, max_n: int,
+                 kernel: int = KERNEL_PRINTED, device=None):
+        L = load_library()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device if isinstance(device, int) else torch.device(device).index)
+        self.G = (int(Gx), int(Gy), int(Gt))
+        self.grid = dict(x0=float(x0), y0=float(y0), t0=float(t0), sres=float(sres), tres=float(tres),
+                         Gx=int(Gx), Gy=int(Gy), Gt=int(Gt), hs=float(hs), ht=float(ht))
+        self.kernel = int(kernel)
+        self.max_n = int(max_n)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(L.stkde_plan_create(ctypes.byref(h), self.device.index, float(x0), float(y0), float(t0),
+                                       float(sres), float(tres), int(Gx), int(Gy), int(Gt), float(hs), float(ht),
+                                       int(kernel), int(max_n)))
+        self._h = h
+
+    # -- lifecycle --
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().stkde_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    # -- compute --
+    def compute(self, points: torch.Tensor, out: Optional[torch.Tensor] = None,
+                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Full grid [Gx, Gy, Gt] float32 (fully overwritten)."""
+        pts = _points_arg(points, self.device)
+        if out is None:
+            out = torch.empty(self.G, dtype=torch.float32, device=self.device)
+        self._check_out(out, self.G[2])
+        _check(load_library().stkde_compute(self._h, pts.data_ptr(), pts.shape[0], out.data_ptr(),
+                                             _stream_ptr(stream, self.device)))
+        return out
+
+    def compute_slab(self, points: torch.Tensor, t_begin: int, t_end: int, n_norm: Optional[int] = None,
+                     out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Time slab [t_begin, t_end): [Gx, Gy, t_end - t_begin] float32, normalised with n_norm."""
+        pts = _points_arg(points, self.device)
+        ts = int(t_end) - int(t_begin)
+        if out is None:
+            out = torch.empty((self.G[0], self.G[1], max(ts, 0)), dtype=torch.float32, device=self.device)
+        self._check_out(out, ts)
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        _check(load_library().stkde_compute_slab(self._h, pts.data_ptr(), pts.shape[0], nn, int(t_begin),
+                                                 int(t_end), out.data_ptr(), _stream_ptr(stream, self.device)))
+        return out
+
+    def _check_out(self, out, ts):
+        if out.device != self.device or out.dtype != torch.float32 or not out.is_contiguous() \
+                or tuple(out.shape) != (self.G[0], self.G[1], ts):
+            raise ValueError("out must be a contiguous float32 CUDA tensor of shape %s"
+                             % ((self.G[0], self.G[1], ts),))
+
+    def slab_partition(self, points: torch.Tensor, nparts: int,
+                       stream: Optional[torch.cuda.Stream] = None) -> list:
+        pts = _points_arg(points, self.device)
+        cuts = (ctypes.c_int64 * (nparts + 1))()
+        _check(load_library().stkde_slab_partition(self._h, pts.data_ptr(), pts.shape[0], int(nparts), cuts,
+                                                   _stream_ptr(stream, self.device)))
+        return [int(c) for c in cuts]
+
+    def count_contributions(self, points: torch.Tensor, t_begin: int = 0, t_end: Optional[int] = None,
+                            stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Exact gated (point, voxel) pair count C as a 1-element int64 device tensor (async)."""
+        pts = _points_arg(points, self.device)
+        out = torch.empty(1, dtype=torch.int64, device=self.device)
+        _check(load_library().stkde_count_contributions(
+            self._h, pts.data_ptr(), pts.shape[0], int(t_begin), int(self.G[2] if t_end is None else t_end),
+            out.data_ptr(), _stream_ptr(stream, self.device)))
+        return out
+
+    # -- diagnostics --
+    def check(self):
+        _check(load_library().stkde_plan_check(self._h))
+
+    def info(self) -> dict:
+        i = PlanInfo()
+        _check(load_library().stkde_plan_info(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in PlanInfo._fields_}
+
+    def enable_kernel_timing(self, on: bool = True):
+        _check(load_library().stkde_plan_enable_kernel_timing(self._h, 1 if on else 0))
+
+    def kernel_ms(self):
+        ms, k = ctypes.c_double(0), ctypes.c_int64(0)
+        _check(load_library().stkde_plan_kernel_ms(self._h, ctypes.byref(ms), ctypes.byref(k)))
+        return ms.value, k.value
+
+
+def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs: Sequence[torch.Tensor],
+                    cuts: Optional[Sequence[int]] = None, root: int = -1,
+                    full: Optional[torch.Tensor] = None, streams=None) -> list:
+    """Single-process multi-device driver (stkde_compute_sharded); returns the cuts used."""
+    L = load_library()
+    nd = len(plans)
+    P = ctypes.c_void_p
+    hp = (P * nd)(*[p.handle.value for p in plans])
+    pts = [_points_arg(x, p.device) for x, p in zip(points, plans)]
+    hpts = (P * nd)(*[x.data_ptr() for x in pts])
+    hsl = (P * nd)(*[s.data_ptr() for s in slabs])
+    hc = (ctypes.c_int64 * (nd + 1))(*([-1] * (nd + 1) if cuts is None else [int(c) for c in cuts]))
+    if streams is None:
+        streams = [torch.cuda.current_stream(p.device) for p in plans]
+    hs = (P * nd)(*[int(s.cuda_stream) for s in streams])
+    _check(L.stkde_compute_sharded(hp, nd, hpts, pts[0].shape[0], hsl, hc, int(root),
+                                   None if full is None else full.data_ptr(), hs))
+    return [int(c) for c in hc]
+
+
+def stkde(points: torch.Tensor, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht,
+          kernel: int = KERNEL_PRINTED) -> torch.Tensor:
+    """One-shot convenience: plan, compute, release."""
+    with Plan(x0=x0, y0=y0, t0=t0, sres=sres, tres=tres, Gx=Gx, Gy=Gy, Gt=Gt, hs=hs, ht=ht,
+              max_n=max(int(points.shape[0]), 1), kernel=kernel, device=points.device.index) as p:
+        out = p.compute(points)
+        torch.cuda.current_stream(points.device).synchronize()
+        return out

@@ -1,0 +1,224 @@
+"""GPU (CUDA, sm_100a) path vs the FP64 oracle, through the C ABI.
+
+Element-wise parity at sizes the oracle finishes in seconds (several tiles,
+ragged tails), sampled parity + exact properties at BASELINE.json's full sizes
+in the launch configuration bench.py times, and the edge cases of the method.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import stkde_synth as synth
+from tests.parity import assert_parity
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _cuda_or_skip():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.fixture(scope="module")
+def S():
+    _cuda_or_skip()
+    import paper_1705_09366_b200 as S
+    S.load_library()
+    return S
+
+
+def run_gpu(S, pts, kernel=0, **g):
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=max(len(pts), 1), kernel=kernel, device=0, **g) as p:
+        t = torch.from_numpy(np.ascontiguousarray(pts, np.float32)).to(dev)
+        out = p.compute(t)
+        c = p.count_contributions(t)
+        torch.cuda.synchronize()
+        p.check()
+        info = p.info()
+        return out.cpu().numpy(), int(c.item()), info
+
+
+def G(Gx, Gy, Gt, res=1.0, hs=3.0, ht=2.0, origin=(0.0, 0.0, 0.0), tres=None):
+    return dict(x0=origin[0], y0=origin[1], t0=origin[2], sres=res, tres=res if tres is None else tres,
+                Gx=Gx, Gy=Gy, Gt=Gt, hs=hs, ht=ht)
+
+
+SMALL = [
+    # name, n, grid, kernel, clustered
+    ("ragged_bt16", 500, G(37, 29, 41, hs=3.0, ht=2.0), 0, True),
+    ("ragged_bt32", 800, G(45, 33, 70, hs=5.5, ht=7.0), 0, True),
+    ("ragged_bt64", 300, G(40, 36, 150, hs=9.0, ht=20.0), 0, False),
+    ("classical", 600, G(33, 47, 35, hs=4.0, ht=3.0), 1, True),
+    ("world_units", 700, G(50, 40, 30, res=0.37, hs=1.5, ht=1.2, origin=(1000.5, -2000.25, 30.0), tres=0.41), 0, True),
+    ("big_disc", 200, G(80, 70, 40, hs=30.0, ht=6.0), 0, False),
+    ("one_voxel_grid", 50, G(1, 1, 1, hs=2.0, ht=2.0), 0, False),
+    ("thin_slab", 400, G(64, 64, 3, hs=4.0, ht=1.0), 0, True),
+]
+
+
+def make_points(n, g, clustered, seed):
+    ext = (g["Gx"] * g["sres"], g["Gy"] * g["sres"], g["Gt"] * g["tres"])
+    if clustered:
+        p = synth.clustered_points(n, 4, 3 * g["sres"], 3 * g["tres"], ext, seed)
+    else:
+        p = synth.uniform_points(n, ext, seed)
+    p = p + np.array([g["x0"], g["y0"], g["t0"]], np.float32)
+    # points outside the box whose cylinders reach in (reading R6)
+    extra = np.array([[g["x0"] - 0.8 * g["hs"], g["y0"] + ext[1] / 2, g["t0"] + ext[2] / 2],
+                      [g["x0"] + ext[0] + 0.5 * g["hs"], g["y0"] - 0.3 * g["hs"], g["t0"] - 0.5 * g["ht"]]],
+                     np.float32)
+    return np.concatenate([p, extra]).astype(np.float32)
+
+
+@pytest.mark.parametrize("case", SMALL, ids=[c[0] for c in SMALL])
+def test_small_full_parity(S, oracle_mod, case):
+    name, n, g, kid, clustered = case
+    pts = make_points(n, g, clustered, seed=len(name))
+    gpu, C, _ = run_gpu(S, pts, kernel=kid, **g)
+    ref = oracle_mod.stkde_pb(pts, kernel=kid, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=name)
+    assert C == ref.contributions
+
+
+@pytest.mark.parametrize("name", ["tiny", "dengue", "social"])
+def test_config_full_parity(S, oracle_mod, name):
+    w = synth.make_config(name)
+    g = w.grid_kwargs()
+    gpu, C, info = run_gpu(S, w.points, **g)
+    ref = oracle_mod.stkde_pb(w.points, **g)
+    rel = assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=name)
+    assert C == ref.contributions
+    print("%s: max |gpu-oracle|/max = %.3e, C = %d, tile %s" % (name, rel, C, (info["Bx"], info["By"], info["Bt"])))
+
+
+def _sample_voxels(gpu, rng, k_top=600, k_rand=600):
+    flat = gpu.reshape(-1)
+    top = np.argpartition(flat, -k_top)[-k_top:]
+    nz = np.flatnonzero(flat > 0)
+    pick = nz[(rng.uniform01(k_rand) * len(nz)).astype(np.int64) % len(nz)]
+    rnd = (rng.uniform01(200) * flat.size).astype(np.int64) % flat.size
+    return np.unique(np.concatenate([top, pick, rnd]))
+
+
+@pytest.mark.parametrize("name", ["ornith", "stress"])
+def test_config_full_size_sampled(S, oracle_mod, name):
+    # BASELINE.json full sizes, the bench.py launch configuration: sampled
+    # voxels (the densest ones, random support voxels, random voxels) against
+    # Alg. 1 evaluated voxel by voxel, plus the exact contribution count.
+    w = synth.make_config(name)
+    g = w.grid_kwargs()
+    gpu, C, _ = run_gpu(S, w.points, **g)
+    vox = _sample_voxels(gpu, synth.SplitMix64(11))
+    val, slack, amb = oracle_mod.stkde_vb_voxels(w.points, vox, **g)
+    vmax = max(val.max(), 0.0)
+    assert_parity(gpu.reshape(-1)[vox], val, slack, amb, vmax=vmax, what=name)
+    assert C == oracle_mod.contributions(w.points, **g)
+
+
+def test_determinism_and_slabs(S):
+    w = synth.make_config("dengue")
+    g = w.grid_kwargs()
+    dev = torch.device("cuda", 0)
+    t = torch.from_numpy(w.points).to(dev)
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        a = p.compute(t).clone()
+        b = p.compute(t).clone()
+        bt = p.info()["Bt"]
+        assert torch.equal(a, b)
+        # Bt-aligned and unaligned slabs equal the corresponding layers bitwise
+        for t0, t1 in [(0, bt), (bt, 3 * bt), (3, 50), (50, 51), (g["Gt"] - 5, g["Gt"])]:
+            s = p.compute_slab(t, t0, t1, n_norm=w.n)
+            assert torch.equal(s, a[:, :, t0:t1]), (t0, t1)
+        cuts = p.slab_partition(t, 4)
+        assert cuts[0] == 0 and cuts[-1] == g["Gt"] and all(c % bt == 0 for c in cuts[:-1])
+        assert all(cuts[i] < cuts[i + 1] for i in range(4))
+
+
+def test_split_hot_tiles(S, oracle_mod):
+    # Force tiny candidate chunks so most tiles split: the last-arriving chunk
+    # sums the partials in chunk order (deterministic, parity-green).
+    w = synth.make_config("dengue")
+    g = w.grid_kwargs()
+    os.environ["STKDE_CHUNK"] = "64"
+    try:
+        gpu, _, info = run_gpu(S, w.points, **g)
+        gpu2, _, _ = run_gpu(S, w.points, **g)
+    finally:
+        del os.environ["STKDE_CHUNK"]
+    assert info["chunk_candidates"] == 64
+    assert np.array_equal(gpu, gpu2)
+    ref = oracle_mod.stkde_pb(w.points, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="split")
+
+
+@pytest.mark.parametrize("bt_c", [(16, 1), (32, 1), (32, 2), (64, 1)])
+def test_tile_variants(S, oracle_mod, bt_c):
+    w = synth.make_config("tiny")
+    g = w.grid_kwargs()
+    os.environ["STKDE_BT"], os.environ["STKDE_C"] = str(bt_c[0]), str(bt_c[1])
+    try:
+        gpu, _, info = run_gpu(S, w.points, **g)
+    finally:
+        del os.environ["STKDE_BT"], os.environ["STKDE_C"]
+    assert info["Bt"] == bt_c[0]
+    ref = oracle_mod.stkde_pb(w.points, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=str(bt_c))
+
+
+def test_sharded_single_process_equals_full(S):
+    # stkde_compute_sharded with every "device" mapped to GPU 0 (fake multi-GPU):
+    # slabs + the peer-memory gather kernel reproduce the full grid bitwise.
+    w = synth.make_config("dengue")
+    g = w.grid_kwargs()
+    dev = torch.device("cuda", 0)
+    t = torch.from_numpy(w.points).to(dev)
+    plans = [S.Plan(max_n=w.n, device=0, **g) for _ in range(3)]
+    try:
+        full_ref = plans[0].compute(t).clone()
+        cuts = plans[0].slab_partition(t, 3)
+        slabs = [torch.empty((g["Gx"], g["Gy"], cuts[i + 1] - cuts[i]), device=dev) for i in range(3)]
+        full = torch.full_like(full_ref, -1.0)
+        used = S.compute_sharded(plans, [t] * 3, slabs, cuts=cuts, root=0, full=full)
+        torch.cuda.synchronize()
+        assert used == cuts
+        assert torch.equal(full, full_ref)
+    finally:
+        for p in plans:
+            p.close()
+
+
+def test_edge_cases(S, oracle_mod):
+    dev = torch.device("cuda", 0)
+    g = G(20, 20, 20, hs=3.0, ht=2.0)
+    # n = 0: zeros, no division
+    with S.Plan(max_n=10, device=0, **g) as p:
+        out = torch.full((20, 20, 20), 7.0, device=dev)
+        p.compute(torch.zeros((0, 3), device=dev), out=out)
+        assert not out.any()
+        # n > max_n -> capacity error
+        with pytest.raises(S.StkdeError) as e:
+            p.compute(torch.zeros((11, 3), device=dev))
+        assert e.value.code == -4
+    # single point at a voxel centre: (3 pi / 8) / (hs^2 ht)
+    pts = np.array([[10.5, 10.5, 10.5]], np.float32)
+    gpu, C, _ = run_gpu(S, pts, **g)
+    assert abs(gpu[10, 10, 10] / (3 * np.pi / 8 / (9 * 2)) - 1) < 1e-6
+    ref = oracle_mod.stkde_pb(pts, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="n=1")
+    # non-finite coordinates are skipped and flagged
+    bad = np.array([[5.0, 5.0, 5.0], [np.nan, 1.0, 1.0], [3.0, np.inf, 2.0]], np.float32)
+    with S.Plan(max_n=3, device=0, **g) as p:
+        out = p.compute(torch.from_numpy(bad).to(dev))
+        with pytest.raises(S.StkdeError) as e:
+            p.check()
+        assert e.value.code == -5
+        ref = oracle_mod.stkde_pb(bad, **g)
+        assert_parity(out.cpu().numpy(), ref.vol, ref.slack, ref.amb, what="nonfinite")
+    # invalid plans
+    for bad_g in (dict(g, sres=0.0), dict(g, hs=-1.0), dict(g, Gt=0)):
+        with pytest.raises(S.StkdeError) as e:
+            S.Plan(max_n=1, device=0, **bad_g)
+        assert e.value.code == -1
