@@ -105,6 +105,13 @@ int stkde_compute_slab(stkde_plan_t plan, const float *d_points, int64_t n,
 int stkde_slab_partition(stkde_plan_t plan, const float *d_points, int64_t n,
                          int nparts, int64_t *h_cuts, void *stream);
 
+/* Host-only half of stkde_slab_partition (no CUDA calls): cuts from a
+ * histogram h_hist_T[0..Gt) of the points' voxel layers T_i (clamped into
+ * [0, Gt)).  Bt is the plan's tile height, Ht = ceil(ht/tres), rs = hs/sres.
+ * Writes h_cuts[0..nparts]; returns STKDE_EINVAL on bad sizes. */
+int stkde_slab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, int Bt, int Ht, double rs,
+                    const int64_t *h_hist_T, int nparts, int64_t *h_cuts);
+
 /* Exact number C of gated (point, voxel) pairs whose voxel lies in layers
  * [t_begin, t_end) -- the "contributions" of the metric.  Writes one int64
  * to d_count (device).  Asynchronous. */
@@ -141,6 +148,7 @@ typedef struct {
     int32_t tile_ctas_per_sm;
     int32_t num_sms;
     int32_t chunk_candidates;
+    int32_t tile_layers_per_thread;   /* CT: each thread owns 4 columns x CT layers */
 } stkde_plan_info_t;
 int stkde_plan_info(stkde_plan_t plan, stkde_plan_info_t *info);
 

@@ -93,14 +93,14 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     // Tile height from the temporal window 2H_t+1.
     int BT = g.Ht >= 16 ? 64 : (g.Ht >= 6 ? 32 : 16);
     BT = env_int("STKDE_BT", BT);
-    int C = BT >= 64 ? 1 : 2;
-    C = env_int("STKDE_C", C);
-    if (tile_smem_bytes(BT, C) == 0) { set_error("unsupported tile shape Bt=%d C=%d", BT, C); free(p); return STKDE_EINVAL; }
+    int CT = BT >= 64 ? 16 : 8;
+    CT = env_int("STKDE_CT", CT);
+    if (tile_smem_bytes(BT, CT) == 0) { set_error("unsupported tile shape Bt=%d CT=%d", BT, CT); free(p); return STKDE_EINVAL; }
     g.BT = BT;
-    p->C = C;
+    p->CT = CT;
     p->kernel = kernel_kind;
     g.kernel = kernel_kind;
-    p->tile_threads = 256 / C;
+    p->tile_threads = tile_threads(BT, CT);
     g.NTX = (int)((Gx + BX - 1) / BX);
     g.NTY = (int)((Gy + BY - 1) / BY);
     g.NTT = (int)((Gt + BT - 1) / BT);
@@ -124,8 +124,8 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     p->chunk = (int)chunk;
     p->max_items = p->ntiles + cand_bound / chunk + 1;
     p->max_slots = 2 * (cand_bound / chunk) + 2;
-    p->smem_bytes = tile_smem_bytes(BT, C);
-    int rc = tile_occupancy(BT, C, kernel_kind, &p->ctas_per_sm);
+    p->smem_bytes = tile_smem_bytes(BT, CT);
+    int rc = tile_occupancy(BT, CT, kernel_kind, &p->ctas_per_sm);
     if (rc != STKDE_OK) { set_error("tile kernel attribute/occupancy query failed"); free(p); return rc; }
     if (p->ctas_per_sm < 1) { set_error("tile kernel does not fit on an SM"); free(p); return STKDE_EINVAL; }
 
@@ -258,7 +258,48 @@ extern "C" int stkde_count_contributions(stkde_plan_t p, const float *d_points, 
 
 // Cost-balanced Bt-aligned cuts: per-layer cost =
 //   Gx*Gy*4 B / B_hbm  +  2 * W(T) / P_fp32,
-// W(T) = (disc columns) * #{points whose window contains T}.
+// W(T) = (disc columns) * #{points whose window contains T}; cuts are taken
+// at tile-layer boundaries where the cumulative cost crosses k/nparts.
+extern "C" int stkde_slab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, int Bt, int Ht, double rs,
+                               const int64_t *h_hist, int nparts, int64_t *h_cuts) {
+    if (!h_cuts || !h_hist || nparts < 1 || Gx < 1 || Gy < 1 || Gt < 1 || Bt < 1 || Ht < 0 || !(rs > 0)) {
+        set_error("bad arguments to stkde_slab_cuts");
+        return STKDE_EINVAL;
+    }
+    const double B_hbm = 6.5e12, P_fp32 = 6.0e13;
+    const double disc = M_PI * rs * rs;
+    std::vector<double> pre(Gt + 1, 0.0);   // prefix of point counts by T_i
+    for (int64_t T = 0; T < Gt; ++T) pre[T + 1] = pre[T] + (double)h_hist[T];
+    const int64_t nblk = (Gt + Bt - 1) / Bt;
+    std::vector<double> cost(nblk, 0.0);
+    for (int64_t T = 0; T < Gt; ++T) {
+        int64_t lo = std::max<int64_t>(T - Ht, 0), hi = std::min<int64_t>(T + Ht, Gt - 1);
+        double w = (pre[hi + 1] - pre[lo]) * disc;
+        cost[T / Bt] += (double)Gx * Gy * 4.0 / B_hbm + 2.0 * w / P_fp32;
+    }
+    std::vector<double> cum(nblk + 1, 0.0);
+    for (int64_t b = 0; b < nblk; ++b) cum[b + 1] = cum[b] + cost[b];
+    const double tot = cum[nblk];
+    h_cuts[0] = 0;
+    int64_t prev = 0;
+    for (int k = 1; k < nparts; ++k) {
+        // first block boundary b with cum[b] >= tot*k/nparts (nearest of the two neighbours)
+        const double target = tot * k / nparts;
+        int64_t b = prev + 1;
+        while (b < nblk && cum[b] < target) ++b;
+        if (b > prev + 1 && (target - cum[b - 1]) < (cum[b] - target)) --b;
+        // keep at least one block per remaining part (when possible)
+        b = std::min<int64_t>(b, nblk - (nparts - k));
+        b = std::max<int64_t>(b, std::min<int64_t>(prev + 1, nblk));
+        h_cuts[k] = std::min<int64_t>(b * Bt, Gt);
+        prev = b;
+    }
+    h_cuts[nparts] = Gt;
+    for (int k = 1; k <= nparts; ++k)
+        if (h_cuts[k] < h_cuts[k - 1]) h_cuts[k] = h_cuts[k - 1];
+    return STKDE_OK;
+}
+
 extern "C" int stkde_slab_partition(stkde_plan_t p, const float *d_points, int64_t n, int nparts, int64_t *h_cuts,
                                     void *stream) {
     if (!p || !h_cuts || nparts < 1) { set_error("bad arguments"); return STKDE_EINVAL; }
@@ -272,35 +313,8 @@ extern "C" int stkde_slab_partition(stkde_plan_t p, const float *d_points, int64
         CK(cudaMemcpyAsync(hist.data(), p->hist_t, g.Gt * sizeof(int), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     }
-    const double B_hbm = 6.5e12, P_fp32 = 6.0e13;
-    const double disc = M_PI * (double)g.rs * g.rs;
-    std::vector<double> pre(g.Gt + 2, 0.0);   // prefix of point counts by T_i
-    for (int T = 0; T < g.Gt; ++T) pre[T + 1] = pre[T] + hist[T];
-    const int nblk = g.NTT;
-    std::vector<double> cost(nblk, 0.0);
-    for (int T = 0; T < g.Gt; ++T) {
-        int lo = std::max(T - g.Ht, 0), hi = std::min(T + g.Ht, g.Gt - 1);
-        double w = (pre[hi + 1] - pre[lo]) * disc;
-        cost[T / g.BT] += (double)g.Gx * g.Gy * 4.0 / B_hbm + 2.0 * w / P_fp32;
-    }
-    double tot = 0;
-    for (double c : cost) tot += c;
-    h_cuts[0] = 0;
-    int b = 0;
-    double acc = 0;
-    for (int k = 1; k < nparts; ++k) {
-        const double target = tot * k / nparts;
-        const int min_b = (int)h_cuts[k - 1] / g.BT + 1;          // at least one tile layer per part
-        const int max_b = nblk - (nparts - k);                      // leave one per remaining part
-        while (b < nblk && (acc + cost[b] * 0.5 < target || b < min_b)) { acc += cost[b]; ++b; }
-        int bb = std::min(std::max(b, min_b), std::max(max_b, min_b));
-        while (b < bb) { acc += cost[b]; ++b; }
-        h_cuts[k] = std::min<int64_t>((int64_t)bb * g.BT, g.Gt);
-    }
-    h_cuts[nparts] = g.Gt;
-    for (int k = 1; k <= nparts; ++k)
-        if (h_cuts[k] < h_cuts[k - 1]) h_cuts[k] = h_cuts[k - 1];
-    return STKDE_OK;
+    std::vector<int64_t> h64(hist.begin(), hist.begin() + g.Gt);
+    return stkde_slab_cuts(g.Gx, g.Gy, g.Gt, g.BT, g.Ht, (double)g.rs, h64.data(), nparts, h_cuts);
 }
 
 extern "C" int stkde_compute_sharded(stkde_plan_t *plans, int ndev, const float *const *d_points, int64_t n,
@@ -377,6 +391,7 @@ extern "C" int stkde_plan_info(stkde_plan_t p, stkde_plan_info_t *info) {
     info->tile_ctas_per_sm = p->ctas_per_sm;
     info->num_sms = p->num_sms;
     info->chunk_candidates = p->chunk;
+    info->tile_layers_per_thread = p->CT;
     return STKDE_OK;
 }
 

@@ -133,7 +133,7 @@ struct stkde_plan_s {
     int num_sms;
     stkde::GridParams g;
     int kernel;
-    int C;                    // columns per thread of the tile kernel
+    int CT;                   // layers per thread of the tile kernel (4 columns x CT)
     int tile_threads;
     int ctas_per_sm;
     int64_t max_n;
@@ -181,7 +181,8 @@ int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_be
 int launch_hist_t(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
 int launch_gather(const float *slab, int64_t Gx, int64_t Gy, int64_t Gt, int64_t t0, int64_t t1,
                   float *full, cudaStream_t st);
-size_t tile_smem_bytes(int BT, int C);
-int tile_occupancy(int BT, int C, int kernel, int *ctas_per_sm);
+size_t tile_smem_bytes(int BT, int CT);
+int tile_occupancy(int BT, int CT, int kernel, int *ctas_per_sm);
+int tile_threads(int BT, int CT);
 void set_error(const char *fmt, ...);
 }  // namespace stkde

@@ -12,12 +12,15 @@
 //                        1/(n hs^2 ht) folded into a_y (as Alg. 3 folds it
 //                        into K_s),
 //        mask[y]         the exact disc chord of row y (16 bits);
-//   3. each thread owns C (x,y) columns and accumulates
+//   3. each thread owns 4 columns (x0..x0+3 of one row y) x CT layers and
+//      accumulates
 //        acc[c][t] += s_c * K_t[t],   s_c = mask ? a_x * a_y : 0
 //      (Alg. 3's stkde += K_s K_t) in FP32 registers with
-//      packed FFMA2, skipping warps whose rows miss the disc and 8-layer
-//      chunks outside the window; after every sub-batch the registers are
-//      added into a shared-memory tile accumulator (two-level summation);
+//      packed FFMA2 (one broadcast LDS.128 of K_t feeds 8 FFMA2); a warp
+//      (8 rows x 16 columns x CT layers) skips points whose window misses its
+//      layers or whose disc misses its rows; after every sub-batch the
+//      registers are added into a shared-memory tile accumulator (two-level
+//      summation);
 //   4. writes every voxel of the tile exactly once (no memset, no atomics on
 //      the grid) with coalesced float4 stores; a split hot tile writes its
 //      partial and the last chunk to arrive sums the partials in chunk order.
@@ -25,28 +28,29 @@
 
 namespace stkde {
 
-template <int BT, int C>
+template <int BT, int CT>
 struct Cfg {
-    static constexpr int NTHR = 256 / C;
+    // Thread tile: 4 consecutive x of one row y, CT consecutive layers.
+    // Warp w: rows [8*(w&1), +8), layer group lg = w>>1 (CT layers).
+    static constexpr int NTHR = 64 * (BT / CT);
     static constexpr int NWARP = NTHR / 32;
     static constexpr int P = 32;                 // points per sub-batch
     static constexpr int CAP = P + NTHR;         // staging ring (records)
     static constexpr int BT4 = BT / 4;
+    static constexpr int CT4 = CT / 4;
     static constexpr int OSTR = BT4 + 1;         // padded accumulator row (float4)
-    static constexpr int CH = 8;                 // layers per temporal chunk
-    static constexpr int NCH = BT / CH;
     // shared-memory carve (bytes)
     static constexpr size_t OFF_OUTER = 0;
     static constexpr size_t SZ_OUTER = 256ull * OSTR * 16;
     static constexpr size_t OFF_KT = OFF_OUTER + SZ_OUTER;
     static constexpr size_t SZ_KT = (size_t)P * BT4 * 16;
-    static constexpr size_t OFF_RING = OFF_KT + SZ_KT;
+    static constexpr size_t OFF_AX = OFF_KT + SZ_KT;
+    static constexpr size_t SZ_AX = (size_t)P * 16 * 4;
+    static constexpr size_t OFF_RING = OFF_AX + SZ_AX;
     static constexpr size_t SZ_RING = (size_t)CAP * sizeof(PointRec);
     static constexpr size_t OFF_ROW = OFF_RING + SZ_RING;
     static constexpr size_t SZ_ROW = (size_t)P * 16 * 8;
-    static constexpr size_t OFF_AX = OFF_ROW + SZ_ROW;
-    static constexpr size_t SZ_AX = (size_t)P * 16 * 4;
-    static constexpr size_t OFF_META = OFF_AX + SZ_AX;
+    static constexpr size_t OFF_META = OFF_ROW + SZ_ROW;
     static constexpr size_t SZ_META = (size_t)P * 4;
     static constexpr size_t OFF_SEG = OFF_META + SZ_META;
     static constexpr size_t SZ_SEG = (size_t)(2 * MAXSEG + 1) * 4;
@@ -59,27 +63,29 @@ __device__ __forceinline__ float2 ffma2(float2 a, float s, float2 c) {
     return __ffma2_rn(a, make_float2(s, s), c);
 }
 
-template <int BT, int C, int KK>
-__global__ void __launch_bounds__(256 / C)
+template <int BT, int CT, int KK>
+__global__ void __launch_bounds__(Cfg<BT, CT>::NTHR, 512 / Cfg<BT, CT>::NTHR)
 k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__restrict__ bucket_begin,
        const int4 *__restrict__ items, const uint64_t *__restrict__ nitems_ptr, int *__restrict__ work_counter,
        uint32_t *__restrict__ arrive, float4 *__restrict__ partials, const int chunk, const int c0,
        const float cnorm, float *__restrict__ out, const int64_t t_begin, const int64_t t_end, const int vec_ok) {
-    using K = Cfg<BT, C>;
+    using K = Cfg<BT, CT>;
     extern __shared__ __align__(16) unsigned char smem[];
     float4 *outer = reinterpret_cast<float4 *>(smem + K::OFF_OUTER);
     float4 *kt4 = reinterpret_cast<float4 *>(smem + K::OFF_KT);
+    float4 *ax4 = reinterpret_cast<float4 *>(smem + K::OFF_AX);
+    float *axt = reinterpret_cast<float *>(smem + K::OFF_AX);
     PointRec *ring = reinterpret_cast<PointRec *>(smem + K::OFF_RING);
     float2 *rowt = reinterpret_cast<float2 *>(smem + K::OFF_ROW);
-    float *axt = reinterpret_cast<float *>(smem + K::OFF_AX);
     int *meta = reinterpret_cast<int *>(smem + K::OFF_META);
     int *seg_start = reinterpret_cast<int *>(smem + K::OFF_SEG);
     int *seg_pref = seg_start + MAXSEG;
     int *misc = reinterpret_cast<int *>(smem + K::OFF_MISC);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int my_y = warp * (2 * C) + (lane * C) / 16;
-    const int my_x0 = (lane * C) % 16;
+    const int my_y = 8 * (warp & 1) + (lane & 7);   // row of the thread's 4 columns
+    const int my_xg = lane >> 3;                     // x group: columns 4*my_xg .. +3
+    const int my_lg = warp >> 1;                     // layer group: layers CT*my_lg .. +CT-1
     const uint32_t nitems = (uint32_t)(*nitems_ptr);
     const int Ts = (int)(t_end - t_begin);
 
@@ -92,10 +98,11 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
         const int ls = item.x, jchunk = item.y, nch = item.z;
         const int ta = ls % g.NTX, tb = (ls / g.NTX) % g.NTY, tc = ls / (g.NTX * g.NTY) + c0;
         const int tX0 = ta * BX, tY0 = tb * BY, tT0 = tc * BT;
-        // layers of this tile that are stored: [lt0, lt1) tile-local
+        // stored layers of this tile, tile-local [lt0, lt1)
         const int lt0 = max(0, (int)(t_begin - tT0));
         const int lt1 = min(BT, (int)min((int64_t)g.Gt, t_end) - tT0);
         const int xn = min(BX, g.Gx - tX0), yn = min(BY, g.Gy - tY0);
+        const int gt1 = min(BT, g.Gt - tT0);         // grid layers of the tile [0, gt1)
 
         // ---- home-bucket segments of this tile ----
         const int a0 = max(ta - g.Ra, 0), a1 = min(ta + g.Ra, g.NTX - 1);
@@ -109,10 +116,7 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
             seg_start[k] = (int)s;
             seg_pref[k + 1] = (int)(e - s);
         }
-        // zero my accumulator rows
-#pragma unroll
-        for (int c = 0; c < C; ++c)
-            for (int q = 0; q < K::OSTR; ++q) outer[(c * K::NTHR + tid) * K::OSTR + q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int q = tid; q < 256 * K::OSTR; q += K::NTHR) outer[q] = make_float4(0.f, 0.f, 0.f, 0.f);
         __syncthreads();
         if (tid == 0) {
             int acc = 0;
@@ -123,9 +127,10 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
         const int total = seg_pref[nseg];
         const int cbeg = jchunk * chunk, cend = min(total, cbeg + chunk);
 
-        // tile rectangle in tile-local column coordinates (acceptance test)
+        // Acceptance uses the tile's grid layers (not the slab), so a slab run
+        // accepts exactly the points of the full run: bitwise equal layers.
         const float xmax = (float)(xn - 1), ymax = (float)(yn - 1);
-        const int Tlo = tT0 + lt0, Thi = tT0 + lt1 - 1;
+        const int Tlo = tT0, Thi = tT0 + gt1 - 1;
 
         int head = 0, tail = 0;
         for (int cb = cbeg; cb < cend; cb += K::NTHR) {
@@ -166,7 +171,7 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
             while (tail - head >= K::P || (cb + K::NTHR >= cend && tail > head)) {
                 const int np = min(K::P, tail - head);
                 // ---------------- per-point invariants (Alg. 3) ----------------
-                for (int e = tid; e < np * K::BT4; e += K::NTHR) {
+                for (int e = tid; e < np * K::BT4; e += K::NTHR) {      // K_t line
                     const int p = e / K::BT4, q = e - p * K::BT4;
                     const PointRec &pr = ring[(head + p) % K::CAP];
                     float v[4];
@@ -181,7 +186,7 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
                     }
                     kt4[p * K::BT4 + q] = make_float4(v[0], v[1], v[2], v[3]);
                 }
-                for (int e = tid; e < np * 16; e += K::NTHR) {
+                for (int e = tid; e < np * 16; e += K::NTHR) {           // a_x
                     const int p = e >> 4, xx = e & 15;
                     const PointRec &pr = ring[(head + p) % K::CAP];
                     float dxv = (float)(tX0 + xx - pr.X) + 0.5f - pr.fx;
@@ -191,7 +196,7 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
                     else av = cnorm * (1.0f - u * u);
                     axt[e] = av;
                 }
-                for (int e = tid; e < np * 16; e += K::NTHR) {
+                for (int e = tid; e < np * 16; e += K::NTHR) {           // a_y and the disc chord
                     const int p = e >> 4, yy = e & 15;
                     const PointRec &pr = ring[(head + p) % K::CAP];
                     float dyv = (float)(tY0 + yy - pr.Y) + 0.5f - pr.fy;
@@ -202,63 +207,62 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
                     uint32_t m = (yy < yn) ? row_mask16(g, pr, tX0, tY0 + yy) : 0u;
                     rowt[e] = make_float2(ay, __uint_as_float(m));
                 }
-                for (int p = tid; p < np; p += K::NTHR) {
+                for (int p = tid; p < np; p += K::NTHR) {                 // active layer groups
                     const PointRec &pr = ring[(head + p) % K::CAP];
-                    // window layers |T + 0.5 - (T_i + ft)| <= rt, widened by one layer
                     float cpos = (float)(pr.T - tT0) + pr.ft - 0.5f;
                     int lo = max((int)floorf(cpos - g.rt) - 1, lt0);
                     int hi = min((int)ceilf(cpos + g.rt) + 1, lt1 - 1);
-                    meta[p] = (lo <= hi) ? ((lo / K::CH) | ((hi / K::CH) << 8)) : 0xFF;
+                    int m = 0;
+                    if (lo <= hi) {
+                        int g0 = lo / CT, g1 = hi / CT;
+                        m = ((2 << g1) - 1) & ~((1 << g0) - 1);
+                    }
+                    meta[p] = m;
                 }
                 __syncthreads();
-                // ---------------- accumulate (Alg. 3 inner loop) ----------------
-                float2 acc2[C][BT / 2];
+                // ---------------- accumulate: acc[c][t] += s_c * K_t[t] ----------------
+                float2 acc2[4][CT / 2];
 #pragma unroll
-                for (int c = 0; c < C; ++c)
+                for (int c = 0; c < 4; ++c)
 #pragma unroll
-                    for (int q = 0; q < BT / 2; ++q) acc2[c][q] = make_float2(0.f, 0.f);
+                    for (int q = 0; q < CT / 2; ++q) acc2[c][q] = make_float2(0.f, 0.f);
+#pragma unroll 1
                 for (int p = 0; p < np; ++p) {
+                    if (!((meta[p] >> my_lg) & 1)) continue;               // window misses my layers
                     const float2 rw = rowt[p * 16 + my_y];
-                    const uint32_t mine = (__float_as_uint(rw.y) >> my_x0) & ((1u << C) - 1u);
-                    const int cr = meta[p];
-                    if (!__any_sync(0xffffffffu, mine != 0u) || (cr & 0xFF) > (cr >> 8)) continue;
-                    const int clo = cr & 0xFF, chi = cr >> 8;
-                    float s[C];
-                    if (C == 2) {
-                        const float2 a2 = *reinterpret_cast<const float2 *>(&axt[p * 16 + my_x0]);
-                        if (KK == STKDE_KERNEL_PRINTED) {
-                            s[0] = (mine & 1u) ? a2.x * rw.x : 0.f;
-                            s[C - 1] = (mine & 2u) ? a2.y * rw.x : 0.f;
-                        } else {
-                            s[0] = (mine & 1u) ? a2.x + rw.x : 0.f;
-                            s[C - 1] = (mine & 2u) ? a2.y + rw.x : 0.f;
-                        }
+                    const uint32_t m4 = (__float_as_uint(rw.y) >> (4 * my_xg)) & 0xFu;
+                    if (!__any_sync(0xffffffffu, m4 != 0u)) continue;      // disc misses my rows
+                    const float4 a4 = ax4[p * 4 + my_xg];
+                    float s[4];
+                    if (KK == STKDE_KERNEL_PRINTED) {
+                        s[0] = (m4 & 1u) ? a4.x * rw.x : 0.f;
+                        s[1] = (m4 & 2u) ? a4.y * rw.x : 0.f;
+                        s[2] = (m4 & 4u) ? a4.z * rw.x : 0.f;
+                        s[3] = (m4 & 8u) ? a4.w * rw.x : 0.f;
                     } else {
-                        const float a1 = axt[p * 16 + my_x0];
-                        if (KK == STKDE_KERNEL_PRINTED) s[0] = mine ? a1 * rw.x : 0.f;
-                        else s[0] = mine ? a1 + rw.x : 0.f;
+                        s[0] = (m4 & 1u) ? a4.x + rw.x : 0.f;
+                        s[1] = (m4 & 2u) ? a4.y + rw.x : 0.f;
+                        s[2] = (m4 & 4u) ? a4.z + rw.x : 0.f;
+                        s[3] = (m4 & 8u) ? a4.w + rw.x : 0.f;
                     }
-                    const float4 *kp = kt4 + p * K::BT4;
+                    const float4 *kp = kt4 + p * K::BT4 + my_lg * K::CT4;
 #pragma unroll
-                    for (int ch = 0; ch < K::NCH; ++ch) {
-                        if (ch >= clo && ch <= chi) {
-                            const float4 k0 = kp[2 * ch], k1 = kp[2 * ch + 1];
+                    for (int q = 0; q < K::CT4; ++q) {
+                        const float4 k = kp[q];
 #pragma unroll
-                            for (int c = 0; c < C; ++c) {
-                                acc2[c][4 * ch + 0] = ffma2(make_float2(k0.x, k0.y), s[c], acc2[c][4 * ch + 0]);
-                                acc2[c][4 * ch + 1] = ffma2(make_float2(k0.z, k0.w), s[c], acc2[c][4 * ch + 1]);
-                                acc2[c][4 * ch + 2] = ffma2(make_float2(k1.x, k1.y), s[c], acc2[c][4 * ch + 2]);
-                                acc2[c][4 * ch + 3] = ffma2(make_float2(k1.z, k1.w), s[c], acc2[c][4 * ch + 3]);
-                            }
+                        for (int c = 0; c < 4; ++c) {
+                            acc2[c][2 * q + 0] = ffma2(make_float2(k.x, k.y), s[c], acc2[c][2 * q + 0]);
+                            acc2[c][2 * q + 1] = ffma2(make_float2(k.z, k.w), s[c], acc2[c][2 * q + 1]);
                         }
                     }
                 }
-                // two-level summation: registers -> shared tile accumulator
+                // two-level summation: registers -> shared tile accumulator [col][t]
 #pragma unroll
-                for (int c = 0; c < C; ++c)
+                for (int c = 0; c < 4; ++c) {
+                    const int col = (4 * my_xg + c) * 16 + my_y;
 #pragma unroll
-                    for (int q = 0; q < K::BT4; ++q) {
-                        float4 &o = outer[(c * K::NTHR + tid) * K::OSTR + q];
+                    for (int q = 0; q < K::CT4; ++q) {
+                        float4 &o = outer[col * K::OSTR + my_lg * K::CT4 + q];
                         float4 v = o;
                         v.x += acc2[c][2 * q].x;
                         v.y += acc2[c][2 * q].y;
@@ -266,22 +270,16 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
                         v.w += acc2[c][2 * q + 1].y;
                         o = v;
                     }
+                }
                 head += np;
                 __syncthreads();
             }
         }
 
         // ---------------- store: every voxel exactly once ----------------
-        // f enumerates the tile as [col][t4]; col -> (c, thread) -> (x, y).
-        auto col_xy = [&](int col, int &x, int &y) {
-            int c = col / K::NTHR, t = col - c * K::NTHR;
-            int w = t >> 5, l = t & 31;
-            y = w * (2 * C) + (l * C) / 16;
-            x = (l * C) % 16 + c;
-        };
+        // f enumerates the tile as [col][t4] with col = x*16 + y.
         auto store4 = [&](int col, int q, float4 v) {
-            int x, y;
-            col_xy(col, x, y);
+            const int x = col >> 4, y = col & 15;
             if (x >= xn || y >= yn) return;
             const int T = tT0 + 4 * q;
             const int64_t rowbase = ((int64_t)(tX0 + x) * g.Gy + (tY0 + y)) * Ts - t_begin;
@@ -336,36 +334,39 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
 typedef void (*tile_fn)(const GridParams, const PointRec *, const uint32_t *, const int4 *, const uint64_t *, int *,
                         uint32_t *, float4 *, int, int, float, float *, int64_t, int64_t, int);
 
-template <int BT, int C, int KK>
-static tile_fn get_fn() { return k_tile<BT, C, KK>; }
+template <int BT, int CT, int KK>
+static tile_fn get_fn() { return k_tile<BT, CT, KK>; }
 
-static tile_fn select(int BT, int C, int KK) {
-#define STKDE_SEL(bt, c)                                                            \
-    if (BT == bt && C == c) return KK ? get_fn<bt, c, 1>() : get_fn<bt, c, 0>();
-    STKDE_SEL(16, 1) STKDE_SEL(16, 2) STKDE_SEL(32, 1) STKDE_SEL(32, 2) STKDE_SEL(64, 1)
+// Supported (Bt, CT) thread tiles; CT = layers per thread.
+#define STKDE_TILES(X) X(16, 4) X(16, 8) X(32, 8) X(32, 16) X(64, 16)
+
+static tile_fn select(int BT, int CT, int KK) {
+#define STKDE_SEL(bt, ct) \
+    if (BT == bt && CT == ct) return KK ? get_fn<bt, ct, 1>() : get_fn<bt, ct, 0>();
+    STKDE_TILES(STKDE_SEL)
 #undef STKDE_SEL
     return nullptr;
 }
 
-size_t tile_smem_bytes(int BT, int C) {
-    switch (BT * 10 + C) {
-        case 161: return Cfg<16, 1>::BYTES;
-        case 162: return Cfg<16, 2>::BYTES;
-        case 321: return Cfg<32, 1>::BYTES;
-        case 322: return Cfg<32, 2>::BYTES;
-        case 641: return Cfg<64, 1>::BYTES;
-    }
+size_t tile_smem_bytes(int BT, int CT) {
+#define STKDE_SM(bt, ct) \
+    if (BT == bt && CT == ct) return Cfg<bt, ct>::BYTES;
+    STKDE_TILES(STKDE_SM)
+#undef STKDE_SM
     return 0;
 }
 
-int tile_occupancy(int BT, int C, int KK, int *ctas_per_sm) {
-    tile_fn f = select(BT, C, KK);
+int tile_threads(int BT, int CT) { return 64 * (BT / CT); }
+
+int tile_occupancy(int BT, int CT, int KK, int *ctas_per_sm) {
+    tile_fn f = select(BT, CT, KK);
     if (!f) return STKDE_EINVAL;
-    size_t smem = tile_smem_bytes(BT, C);
+    size_t smem = tile_smem_bytes(BT, CT);
     if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
         return STKDE_ECUDA;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, 256 / C, smem) != cudaSuccess) return STKDE_ECUDA;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, f, tile_threads(BT, CT), smem) != cudaSuccess)
+        return STKDE_ECUDA;
     *ctas_per_sm = occ;
     return STKDE_OK;
 }
@@ -373,7 +374,7 @@ int tile_occupancy(int BT, int C, int KK, int *ctas_per_sm) {
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float cnorm, float *out,
                 cudaStream_t st) {
     const GridParams &g = p->g;
-    tile_fn f = select(g.BT, p->C, p->kernel);
+    tile_fn f = select(g.BT, p->CT, p->kernel);
     if (!f) return STKDE_EINVAL;
     const int nsl = g.NTX * g.NTY * (c1 - c0);
     const int64_t Ts = t_end - t_begin;

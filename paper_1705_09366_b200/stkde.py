@@ -21,7 +21,7 @@ KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
 
 # Exported entry points of include/stkde.h (checked by tests/test_abi.py).
 EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_compute_slab",
-           "stkde_slab_partition", "stkde_count_contributions", "stkde_compute_sharded",
+           "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
            "stkde_plan_kernel_ms", "stkde_strerror", "stkde_last_error")
 
@@ -38,7 +38,8 @@ class PlanInfo(ctypes.Structure):
                 ("ntiles", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("last_own_launches", ctypes.c_int32), ("last_cub_calls", ctypes.c_int32),
                 ("tile_threads", ctypes.c_int32), ("tile_ctas_per_sm", ctypes.c_int32),
-                ("num_sms", ctypes.c_int32), ("chunk_candidates", ctypes.c_int32)]
+                ("num_sms", ctypes.c_int32), ("chunk_candidates", ctypes.c_int32),
+                ("tile_layers_per_thread", ctypes.c_int32)]
 
 
 _lib = None
@@ -59,6 +60,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_compute.argtypes = [P, P, I64, P, P]
     L.stkde_compute_slab.argtypes = [P, P, I64, I64, I64, I64, P, P]
     L.stkde_slab_partition.argtypes = [P, P, I64, I32, ctypes.POINTER(I64), P]
+    L.stkde_slab_cuts.argtypes = [I64, I64, I64, I32, I32, D, ctypes.POINTER(I64), I32, ctypes.POINTER(I64)]
     L.stkde_count_contributions.argtypes = [P, P, I64, I64, I64, P, P]
     L.stkde_compute_sharded.argtypes = [ctypes.POINTER(P), I32, ctypes.POINTER(P), I64, ctypes.POINTER(P),
                                         ctypes.POINTER(I64), I32, P, ctypes.POINTER(P)]
@@ -70,7 +72,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
     L.stkde_last_error.restype = ctypes.c_char_p
-    for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition",
+    for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition", "stkde_slab_cuts",
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms"):
         getattr(L, name).restype = I32
@@ -226,6 +228,16 @@ def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs
     _check(L.stkde_compute_sharded(hp, nd, hpts, pts[0].shape[0], hsl, hc, int(root),
                                    None if full is None else full.data_ptr(), hs))
     return [int(c) for c in hc]
+
+
+def slab_cuts(G, Bt: int, Ht: int, rs: float, hist_T, nparts: int) -> list:
+    """Host-only cost-balanced Bt-aligned cuts from a layer histogram (stkde_slab_cuts)."""
+    L = load_library()
+    Gt = int(G[2])
+    h = (ctypes.c_int64 * Gt)(*[int(v) for v in hist_T])
+    cuts = (ctypes.c_int64 * (nparts + 1))()
+    _check(L.stkde_slab_cuts(int(G[0]), int(G[1]), Gt, int(Bt), int(Ht), float(rs), h, int(nparts), cuts))
+    return [int(c) for c in cuts]
 
 
 def stkde(points: torch.Tensor, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht,

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import stkde_synth as synth
-from tests.parity import assert_parity
+from parity import assert_parity
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -154,15 +154,15 @@ def test_split_hot_tiles(S, oracle_mod):
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="split")
 
 
-@pytest.mark.parametrize("bt_c", [(16, 1), (32, 1), (32, 2), (64, 1)])
+@pytest.mark.parametrize("bt_c", [(16, 4), (16, 8), (32, 8), (32, 16), (64, 16)])
 def test_tile_variants(S, oracle_mod, bt_c):
     w = synth.make_config("tiny")
     g = w.grid_kwargs()
-    os.environ["STKDE_BT"], os.environ["STKDE_C"] = str(bt_c[0]), str(bt_c[1])
+    os.environ["STKDE_BT"], os.environ["STKDE_CT"] = str(bt_c[0]), str(bt_c[1])
     try:
         gpu, _, info = run_gpu(S, w.points, **g)
     finally:
-        del os.environ["STKDE_BT"], os.environ["STKDE_C"]
+        del os.environ["STKDE_BT"], os.environ["STKDE_CT"]
     assert info["Bt"] == bt_c[0]
     ref = oracle_mod.stkde_pb(w.points, **g)
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=str(bt_c))
