@@ -41,9 +41,9 @@ UNIT = "contributions/s"
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x 2 x max SM clock
 CONFIG_INDEX = {"tiny": 0, "dengue": 1, "social": 2, "ornith": 3, "stress": 4}
 # oracle sample sizes for the cpu_baseline / reference legs (about 10-30 s of host work)
-ORACLE_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 200000, "ornith": 150000, "stress": 20000}
+ORACLE_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 600000, "ornith": 1000000, "stress": 150000}
 # per-step sample of the --impl reference arm (a few seconds per step, so K steps end in minutes)
-REF_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 50000, "ornith": 30000, "stress": 4000}
+REF_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 200000, "ornith": 200000, "stress": 20000}
 
 
 def peaks():
