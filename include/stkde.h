@@ -60,6 +60,12 @@ enum {
     STKDE_KERNEL_CLASSICAL = 1  /* k_s = 2/pi (1-u^2-v^2),     k_t = 3/4 (1-w^2)                    */
 };
 
+/* Tile-kernel engine (environment variable STKDE_ENGINE at plan creation;
+ * default TENSOR).  SIMT: FP32 FFMA2 accumulation in registers.  TENSOR: the
+ * per-tile contraction on tensor cores (mma.sync m16n8k16, FP16 3-term split,
+ * FP32 accumulation) -- DESIGN.md §3.5. */
+enum { STKDE_ENGINE_SIMT = 0, STKDE_ENGINE_TENSOR = 1 };
+
 typedef struct stkde_plan_s *stkde_plan_t;
 
 /* Create a plan on `device` (CUDA ordinal).  Grid origin (x0,y0,t0), voxel
@@ -148,7 +154,8 @@ typedef struct {
     int32_t tile_ctas_per_sm;
     int32_t num_sms;
     int32_t chunk_candidates;
-    int32_t tile_layers_per_thread;   /* CT: each thread owns 4 columns x CT layers */
+    int32_t tile_layers_per_thread;   /* CT: each thread owns 4 columns x CT layers (SIMT engine) */
+    int32_t engine;                   /* STKDE_ENGINE_* of the tile kernel */
 } stkde_plan_info_t;
 int stkde_plan_info(stkde_plan_t plan, stkde_plan_info_t *info);
 

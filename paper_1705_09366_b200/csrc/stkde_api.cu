@@ -124,8 +124,17 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     p->chunk = (int)chunk;
     p->max_items = p->ntiles + cand_bound / chunk + 1;
     p->max_slots = 2 * (cand_bound / chunk) + 2;
-    p->smem_bytes = tile_smem_bytes(BT, CT);
-    int rc = tile_occupancy(BT, CT, kernel_kind, &p->ctas_per_sm);
+    p->engine = env_int("STKDE_ENGINE", STKDE_ENGINE_TENSOR);
+    if (p->engine != STKDE_ENGINE_SIMT && p->engine != STKDE_ENGINE_TENSOR) { set_error("bad STKDE_ENGINE"); free(p); return STKDE_EINVAL; }
+    int rc;
+    if (p->engine == STKDE_ENGINE_TENSOR) {
+        p->tile_threads = 256;
+        p->smem_bytes = tile_mma_smem_bytes(BT);
+        rc = tile_mma_occupancy(BT, kernel_kind, &p->ctas_per_sm);
+    } else {
+        p->smem_bytes = tile_smem_bytes(BT, CT);
+        rc = tile_occupancy(BT, CT, kernel_kind, &p->ctas_per_sm);
+    }
     if (rc != STKDE_OK) { set_error("tile kernel attribute/occupancy query failed"); free(p); return rc; }
     if (p->ctas_per_sm < 1) { set_error("tile kernel does not fit on an SM"); free(p); return STKDE_EINVAL; }
 
@@ -229,7 +238,8 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
     const int c0 = (int)(t_begin / g.BT), c1 = (int)((t_end + g.BT - 1) / g.BT);
     rc = launch_worklist(p, c0, c1, st);
     if (rc) { set_error("work-list launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
-    rc = launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
+    rc = p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
+                                          : launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
     if (rc) { set_error("tile kernel launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     return STKDE_OK;
 }
@@ -392,6 +402,7 @@ extern "C" int stkde_plan_info(stkde_plan_t p, stkde_plan_info_t *info) {
     info->num_sms = p->num_sms;
     info->chunk_candidates = p->chunk;
     info->tile_layers_per_thread = p->CT;
+    info->engine = p->engine;
     return STKDE_OK;
 }
 

@@ -134,6 +134,7 @@ struct stkde_plan_s {
     stkde::GridParams g;
     int kernel;
     int CT;                   // layers per thread of the tile kernel (4 columns x CT)
+    int engine;               // STKDE_ENGINE_*: 0 = FP32 FFMA2 (SIMT), 1 = tensor-core mma.sync 3xFP16
     int tile_threads;
     int ctas_per_sm;
     int64_t max_n;
@@ -184,5 +185,9 @@ int launch_gather(const float *slab, int64_t Gx, int64_t Gy, int64_t Gt, int64_t
 size_t tile_smem_bytes(int BT, int CT);
 int tile_occupancy(int BT, int CT, int kernel, int *ctas_per_sm);
 int tile_threads(int BT, int CT);
+size_t tile_mma_smem_bytes(int BT);
+int tile_mma_occupancy(int BT, int kernel, int *ctas_per_sm);
+int launch_tile_mma(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float cscale, float *out,
+                    cudaStream_t st);
 void set_error(const char *fmt, ...);
 }  // namespace stkde

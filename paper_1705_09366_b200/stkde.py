@@ -39,7 +39,7 @@ class PlanInfo(ctypes.Structure):
                 ("last_own_launches", ctypes.c_int32), ("last_cub_calls", ctypes.c_int32),
                 ("tile_threads", ctypes.c_int32), ("tile_ctas_per_sm", ctypes.c_int32),
                 ("num_sms", ctypes.c_int32), ("chunk_candidates", ctypes.c_int32),
-                ("tile_layers_per_thread", ctypes.c_int32)]
+                ("tile_layers_per_thread", ctypes.c_int32), ("engine", ctypes.c_int32)]
 
 
 _lib = None

@@ -33,7 +33,7 @@ for name in names:
         kms, kl = p.kernel_ms()
         info = p.info()
         p.check()
-        print("%-7s n=%-8d C=%.3e  step %.3f ms  tile kernel %.3f ms  -> %.3e contrib/s  tile=%dx%dx%d CT=%d occ=%d chunk=%d launches=%d+%dcub"
+        print("%-7s n=%-8d C=%.3e  step %.3f ms  tile kernel %.3f ms  -> %.3e contrib/s  tile=%dx%dx%d CT=%d occ=%d chunk=%d launches=%d+%dcub eng=%d"
               % (name, w.n, C, ms, kms / max(kl, 1), C / (ms * 1e-3), info["Bx"], info["By"], info["Bt"],
                  info["tile_layers_per_thread"], info["tile_ctas_per_sm"], info["chunk_candidates"],
-                 info["last_own_launches"], info["last_cub_calls"]), flush=True)
+                 info["last_own_launches"], info["last_cub_calls"], info["engine"]), flush=True)

@@ -73,18 +73,30 @@ def make_points(n, g, clustered, seed):
     return np.concatenate([p, extra]).astype(np.float32)
 
 
+@pytest.fixture(params=[1, 0], ids=["tensor", "simt"])
+def engine(request):
+    old = os.environ.get("STKDE_ENGINE")
+    os.environ["STKDE_ENGINE"] = str(request.param)
+    yield request.param
+    if old is None:
+        del os.environ["STKDE_ENGINE"]
+    else:
+        os.environ["STKDE_ENGINE"] = old
+
+
 @pytest.mark.parametrize("case", SMALL, ids=[c[0] for c in SMALL])
-def test_small_full_parity(S, oracle_mod, case):
+def test_small_full_parity(S, oracle_mod, case, engine):
     name, n, g, kid, clustered = case
     pts = make_points(n, g, clustered, seed=len(name))
-    gpu, C, _ = run_gpu(S, pts, kernel=kid, **g)
+    gpu, C, info = run_gpu(S, pts, kernel=kid, **g)
+    assert info["engine"] == engine
     ref = oracle_mod.stkde_pb(pts, kernel=kid, **g)
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=name)
     assert C == ref.contributions
 
 
 @pytest.mark.parametrize("name", ["tiny", "dengue", "social"])
-def test_config_full_parity(S, oracle_mod, name):
+def test_config_full_parity(S, oracle_mod, name, engine):
     w = synth.make_config(name)
     g = w.grid_kwargs()
     gpu, C, info = run_gpu(S, w.points, **g)
@@ -118,7 +130,7 @@ def test_config_full_size_sampled(S, oracle_mod, name):
     assert C == oracle_mod.contributions(w.points, **g)
 
 
-def test_determinism_and_slabs(S):
+def test_determinism_and_slabs(S, engine):
     w = synth.make_config("dengue")
     g = w.grid_kwargs()
     dev = torch.device("cuda", 0)
@@ -137,7 +149,7 @@ def test_determinism_and_slabs(S):
         assert all(cuts[i] < cuts[i + 1] for i in range(4))
 
 
-def test_split_hot_tiles(S, oracle_mod):
+def test_split_hot_tiles(S, oracle_mod, engine):
     # Force tiny candidate chunks so most tiles split: the last-arriving chunk
     # sums the partials in chunk order (deterministic, parity-green).
     w = synth.make_config("dengue")
@@ -158,11 +170,11 @@ def test_split_hot_tiles(S, oracle_mod):
 def test_tile_variants(S, oracle_mod, bt_c):
     w = synth.make_config("tiny")
     g = w.grid_kwargs()
-    os.environ["STKDE_BT"], os.environ["STKDE_CT"] = str(bt_c[0]), str(bt_c[1])
+    os.environ["STKDE_BT"], os.environ["STKDE_CT"], os.environ["STKDE_ENGINE"] = str(bt_c[0]), str(bt_c[1]), "0"
     try:
         gpu, _, info = run_gpu(S, w.points, **g)
     finally:
-        del os.environ["STKDE_BT"], os.environ["STKDE_CT"]
+        del os.environ["STKDE_BT"], os.environ["STKDE_CT"], os.environ["STKDE_ENGINE"]
     assert info["Bt"] == bt_c[0]
     ref = oracle_mod.stkde_pb(w.points, **g)
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=str(bt_c))
