@@ -21,7 +21,11 @@ constexpr int BY = 16;            // tile width in Y (voxels)
 constexpr int MAXSEG = 256;       // max home-bucket segments per tile
 // Relative band around the disc edge inside which the FP32 gate defers to
 // the exact FP64 expression (reading R13): |d^2 - r^2| <= BAND r^2.
-constexpr float GATE_BAND = 1e-4f;
+// The FP32 voxel-local d^2 is within ~3e-7 (relative) of the FP64 value, so
+// 4e-6 leaves a >10x margin while keeping FP64 evaluations rare.
+constexpr float GATE_BAND = 4e-6f;
+// Conservative margin of the tile acceptance test (culling only).
+constexpr float CULL_BAND = 1e-4f;
 
 // Per-point record written by the prep kernel (32 B, one per input point).
 //   X, Y, T     voxel of the point: floor((x - x0)/sres) ...

@@ -149,7 +149,7 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
                     float py = (float)(r.Y - tY0) + r.fy - 0.5f;
                     float dx = fminf(fmaxf(px, 0.f), xmax) - px;
                     float dy = fminf(fmaxf(py, 0.f), ymax) - py;
-                    acc = dx * dx + dy * dy < g.rs2 * (1.0f + GATE_BAND) + 1e-6f;
+                    acc = dx * dx + dy * dy < g.rs2 * (1.0f + CULL_BAND) + 1e-6f;
                 }
             }
             const unsigned bal = __ballot_sync(0xffffffffu, acc);

@@ -41,7 +41,11 @@ struct CfgM {
     static constexpr size_t SZ_RING = (size_t)CAP * sizeof(PointRec);
     static constexpr size_t OFF_META = OFF_RING + SZ_RING;
     static constexpr size_t SZ_META = (size_t)P * 4;
-    static constexpr size_t OFF_SEG = OFF_META + SZ_META;
+    static constexpr size_t OFF_BREC = OFF_META + SZ_META;       // linearised sub-batch
+    static constexpr size_t SZ_BREC = (size_t)P * sizeof(PointRec);
+    static constexpr size_t OFF_BP = OFF_BREC + SZ_BREC;         // bpx, bpy, bpt [P] each
+    static constexpr size_t SZ_BP = (size_t)3 * P * 4;
+    static constexpr size_t OFF_SEG = OFF_BP + SZ_BP;
     static constexpr size_t SZ_SEG = (size_t)(2 * MAXSEG + 1) * 4;
     static constexpr size_t OFF_MISC = OFF_SEG + SZ_SEG;
     static constexpr size_t SZ_MISC = 64 * 4;
@@ -77,7 +81,7 @@ __device__ __forceinline__ void split2(float v0, float v1, uint32_t &hi, uint32_
 }
 
 template <int BT, int KK>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, (BT <= 16 ? 3 : 2))
 k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__restrict__ bucket_begin,
            const int4 *__restrict__ items, const uint64_t *__restrict__ nitems_ptr, int *__restrict__ work_counter,
            uint32_t *__restrict__ arrive, float4 *__restrict__ partials, const int chunk, const int c0,
@@ -91,6 +95,10 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
     float2 *rowT = reinterpret_cast<float2 *>(smem + K::OFF_ROW);
     PointRec *ring = reinterpret_cast<PointRec *>(smem + K::OFF_RING);
     int *meta = reinterpret_cast<int *>(smem + K::OFF_META);
+    PointRec *brec = reinterpret_cast<PointRec *>(smem + K::OFF_BREC);
+    float *bpx = reinterpret_cast<float *>(smem + K::OFF_BP);
+    float *bpy = bpx + K::P;
+    float *bpt = bpy + K::P;
     int *seg_start = reinterpret_cast<int *>(smem + K::OFF_SEG);
     int *seg_pref = seg_start + MAXSEG;
     int *misc = reinterpret_cast<int *>(smem + K::OFF_MISC);
@@ -100,8 +108,8 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
     const uint32_t nitems = (uint32_t)(*nitems_ptr);
     const int Ts = (int)(t_end - t_begin);
 
+    if (tid == 0) misc[0] = atomicAdd(work_counter, 1);
     for (;;) {
-        if (tid == 0) misc[0] = atomicAdd(work_counter, 1);
         __syncthreads();
         const uint32_t it = (uint32_t)misc[0];
         if (it >= nitems) break;
@@ -126,10 +134,10 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
             seg_start[k] = (int)s;
             seg_pref[k + 1] = (int)(e - s);
         }
-        for (int q = tid; q < 256 * K::RS / 4; q += K::NTHR)
-            reinterpret_cast<float4 *>(outer)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+        bool touched = false;   // the shared accumulator holds data (no zero-fill pass)
         __syncthreads();
         if (tid == 0) {
+            misc[0] = atomicAdd(work_counter, 1);   // next item, fetched while this one runs
             int acc = 0;
             seg_pref[0] = 0;
             for (int k = 0; k < nseg; ++k) { acc += seg_pref[k + 1]; seg_pref[k + 1] = acc; }
@@ -157,7 +165,7 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                     float py = (float)(r.Y - tY0) + r.fy - 0.5f;
                     float dx = fminf(fmaxf(px, 0.f), xmax) - px;
                     float dy = fminf(fmaxf(py, 0.f), ymax) - py;
-                    acc = dx * dx + dy * dy < g.rs2 * (1.0f + GATE_BAND) + 1e-6f;
+                    acc = dx * dx + dy * dy < g.rs2 * (1.0f + CULL_BAND) + 1e-6f;
                 }
             }
             const unsigned bal = __ballot_sync(0xffffffffu, acc);
@@ -179,25 +187,42 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
             while (tail - head >= K::P || (cb + K::NTHR >= cend && tail > head)) {
                 const int np = min(K::P, tail - head);
                 // ---------------- per-point invariants, operand layouts ----------------
-                // K_t in B-fragment order: [k-step][n-tile][lane] = {hi(k0,k0+1), hi(k0+8,k0+9), lo.., lo..}
+                // (1) linearise the sub-batch: tile-local continuous coordinates of
+                //     each point (column x is at offset x - px) and its n-tile mask.
+                for (int p = tid; p < K::P; p += K::NTHR) {
+                    int m = 0;
+                    float4 q = make_float4(1e30f, 1e30f, 1e30f, 0.f);      // padding: far away
+                    if (p < np) {
+                        const PointRec pr = ring[(head + p) % K::CAP];
+                        brec[p] = pr;
+                        q = make_float4((float)(pr.X - tX0) + pr.fx - 0.5f, (float)(pr.Y - tY0) + pr.fy - 0.5f,
+                                        (float)(pr.T - tT0) + pr.ft - 0.5f, 0.f);
+                        int lo = max((int)floorf(q.z - g.rt) - 1, lt0);
+                        int hi = min((int)ceilf(q.z + g.rt) + 1, lt1 - 1);
+                        if (lo <= hi) m = ((2 << (hi >> 3)) - 1) & ~((1 << (lo >> 3)) - 1);
+                    }
+                    bpx[p] = q.x;
+                    bpy[p] = q.y;
+                    bpt[p] = q.z;
+                    meta[p] = m;
+                }
+                __syncthreads();
+                // (2) K_t in B-fragment order: [k-step][n-tile][lane] = {hi(k0,k0+1), hi(k0+8,k0+9), lo.., lo..}
                 for (int e = tid; e < K::KS * K::NT * 32; e += K::NTHR) {
                     const int l = e & 31, nt = (e >> 5) % K::NT, ks = (e >> 5) / K::NT;
-                    const int layer = 8 * nt + (l >> 2);
+                    const float layer = (float)(8 * nt + (l >> 2));
                     const int pb = 16 * ks + 2 * (l & 3);
+                    const float2 t01 = *reinterpret_cast<const float2 *>(&bpt[pb]);
+                    const float2 t89 = *reinterpret_cast<const float2 *>(&bpt[pb + 8]);
+                    const float tp[4] = {t01.x, t01.y, t89.x, t89.y};
                     float v[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
-                        const int p = pb + (j & 1) + 8 * (j >> 1);
-                        float kv = 0.f;
-                        if (p < np) {
-                            const PointRec &pr = ring[(head + p) % K::CAP];
-                            float dtv = (float)(tT0 + layer - pr.T) + 0.5f - pr.ft;
-                            float w = fabsf(dtv) * g.inv_rt;
-                            if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - w; kv = 0.75f * (a * a); }
-                            else kv = 0.75f * (1.0f - w * w);
-                            kv = (w <= 1.0f) ? kv : 0.0f;
-                        }
-                        v[j] = fp16_range(kv);
+                        float w = fabsf(layer - tp[j]) * g.inv_rt;
+                        float kv;
+                        if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - w; kv = 0.75f * (a * a); }
+                        else kv = 0.75f * (1.0f - w * w);
+                        v[j] = fp16_range((w <= 1.0f) ? kv : 0.0f);
                     }
                     uint4 f;
                     split2(v[0], v[1], f.x, f.z);
@@ -206,40 +231,23 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                 }
                 for (int e = tid; e < 16 * K::P; e += K::NTHR) {           // a_x, transposed [x][p]
                     const int p = e & (K::P - 1), xx = e / K::P;
-                    float av = 0.f;
-                    if (p < np) {
-                        const PointRec &pr = ring[(head + p) % K::CAP];
-                        float dxv = (float)(tX0 + xx - pr.X) + 0.5f - pr.fx;
-                        float u = fabsf(dxv) * g.inv_rs;
-                        if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - u; av = a * a; }
-                        else av = 1.0f - u * u;
-                    }
-                    axT[xx * K::AXS + p] = av;
+                    float u = fabsf((float)xx - bpx[p]) * g.inv_rs;
+                    float av;
+                    if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - u; av = a * a; }
+                    else av = 1.0f - u * u;
+                    axT[xx * K::AXS + p] = (p < np) ? av : 0.f;
                 }
                 for (int e = tid; e < 16 * K::P; e += K::NTHR) {           // a_y and the chord, [y][p]
                     const int p = e & (K::P - 1), yy = e / K::P;
                     float ay = 0.f;
                     uint32_t m = 0u;
                     if (p < np) {
-                        const PointRec &pr = ring[(head + p) % K::CAP];
-                        float dyv = (float)(tY0 + yy - pr.Y) + 0.5f - pr.fy;
-                        float v = fabsf(dyv) * g.inv_rs;
+                        float v = fabsf((float)yy - bpy[p]) * g.inv_rs;
                         if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - v; ay = a * a; }
                         else ay = -(v * v);
-                        m = (yy < yn) ? row_mask16(g, pr, tX0, tY0 + yy) : 0u;
+                        if (yy < yn && v < 1.0f + CULL_BAND) m = row_mask16(g, brec[p], tX0, tY0 + yy);
                     }
                     rowT[e] = make_float2(ay, __uint_as_float(m));
-                }
-                for (int p = tid; p < K::P; p += K::NTHR) {                // n-tiles of each window
-                    int m = 0;
-                    if (p < np) {
-                        const PointRec &pr = ring[(head + p) % K::CAP];
-                        float cpos = (float)(pr.T - tT0) + pr.ft - 0.5f;
-                        int lo = max((int)floorf(cpos - g.rt) - 1, lt0);
-                        int hi = min((int)ceilf(cpos + g.rt) + 1, lt1 - 1);
-                        if (lo <= hi) m = ((2 << (hi >> 3)) - 1) & ~((1 << (lo >> 3)) - 1);
-                    }
-                    meta[p] = m;
                 }
                 __syncthreads();
                 // ---------------- tensor-core accumulation ----------------
@@ -254,16 +262,24 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                 for (int ks = 0; ks < K::KS; ++ks) {
                     const int ntm = __reduce_or_sync(0xffffffffu, lane < 16 ? meta[16 * ks + lane] : 0);
                     if (ntm == 0) continue;
-                    uint32_t ahi[2][4], alo[2][4];
+                    uint32_t ahi[2][4] = {}, alo[2][4] = {};
                     bool act[2];
+                    float4 r01v[2], r89v[2];
 #pragma unroll
                     for (int mt = 0; mt < 2; ++mt) {
                         const int y = 2 * warp + mt;
-                        const float4 r01 = *reinterpret_cast<const float4 *>(&rowT[y * K::P + 16 * ks + 2 * tq]);
-                        const float4 r89 = *reinterpret_cast<const float4 *>(&rowT[y * K::P + 16 * ks + 2 * tq + 8]);
+                        r01v[mt] = *reinterpret_cast<const float4 *>(&rowT[y * K::P + 16 * ks + 2 * tq]);
+                        r89v[mt] = *reinterpret_cast<const float4 *>(&rowT[y * K::P + 16 * ks + 2 * tq + 8]);
+                        act[mt] = __any_sync(0xffffffffu, (__float_as_uint(r01v[mt].y) | __float_as_uint(r01v[mt].w) |
+                                                           __float_as_uint(r89v[mt].y) | __float_as_uint(r89v[mt].w)) != 0u);
+                    }
+                    if (!act[0] && !act[1]) continue;
+#pragma unroll
+                    for (int mt = 0; mt < 2; ++mt) {
+                        if (!act[mt]) continue;            // row misses all 16 discs: no A fragment
+                        const float4 r01 = r01v[mt], r89 = r89v[mt];
                         const uint32_t m0 = __float_as_uint(r01.y), m1 = __float_as_uint(r01.w);
                         const uint32_t m8 = __float_as_uint(r89.y), m9 = __float_as_uint(r89.w);
-                        act[mt] = __any_sync(0xffffffffu, (m0 | m1 | m8 | m9) != 0u);
                         const float2 ag01 = *reinterpret_cast<const float2 *>(&axT[gq * K::AXS + 16 * ks + 2 * tq]);
                         const float2 ag89 = *reinterpret_cast<const float2 *>(&axT[gq * K::AXS + 16 * ks + 2 * tq + 8]);
                         const float2 aG01 = *reinterpret_cast<const float2 *>(&axT[(gq + 8) * K::AXS + 16 * ks + 2 * tq]);
@@ -296,7 +312,6 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                         split2(s[4], s[5], ahi[mt][2], alo[mt][2]);
                         split2(s[6], s[7], ahi[mt][3], alo[mt][3]);
                     }
-                    if (!act[0] && !act[1]) continue;
 #pragma unroll
                     for (int nt = 0; nt < K::NT; ++nt) {
                         if (!((ntm >> nt) & 1)) continue;
@@ -318,15 +333,18 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                     for (int nt = 0; nt < K::NT; ++nt) {
                         float2 *o0 = reinterpret_cast<float2 *>(&outer[(y * 16 + gq) * K::RS + 8 * nt + 2 * tq]);
                         float2 *o1 = reinterpret_cast<float2 *>(&outer[(y * 16 + gq + 8) * K::RS + 8 * nt + 2 * tq]);
-                        float2 v0 = *o0, v1 = *o1;
-                        v0.x += cacc[mt][nt][0];
-                        v0.y += cacc[mt][nt][1];
-                        v1.x += cacc[mt][nt][2];
-                        v1.y += cacc[mt][nt][3];
+                        float2 v0 = make_float2(cacc[mt][nt][0], cacc[mt][nt][1]);
+                        float2 v1 = make_float2(cacc[mt][nt][2], cacc[mt][nt][3]);
+                        if (touched) {       // first sub-batch writes, later ones add
+                            const float2 u0 = *o0, u1 = *o1;
+                            v0.x += u0.x; v0.y += u0.y;
+                            v1.x += u1.x; v1.y += u1.y;
+                        }
                         *o0 = v0;
                         *o1 = v1;
                     }
                 }
+                touched = true;
                 head += np;
                 __syncthreads();
             }
@@ -353,17 +371,18 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
         constexpr int BT4 = BT / 4;
         constexpr int NF = 256 * BT4;
         const float4 *outer4 = reinterpret_cast<const float4 *>(outer);
+        const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if (nch == 1) {
             for (int f = tid; f < NF; f += K::NTHR) {
                 int col = f / BT4, q = f - col * BT4;
-                store4(col, q, outer4[col * (K::RS / 4) + q]);
+                store4(col, q, touched ? outer4[col * (K::RS / 4) + q] : zero4);
             }
         } else {
             const int slot0 = item.w;
             float4 *mine = partials + (size_t)(slot0 + jchunk) * NF;
             for (int f = tid; f < NF; f += K::NTHR) {
                 int col = f / BT4, q = f - col * BT4;
-                mine[f] = outer4[col * (K::RS / 4) + q];
+                mine[f] = touched ? outer4[col * (K::RS / 4) + q] : zero4;
             }
             __threadfence();
             __syncthreads();
