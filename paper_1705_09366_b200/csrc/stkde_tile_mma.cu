@@ -25,6 +25,7 @@ struct CfgM {
     static constexpr int NWARP = 8;
     static constexpr int P = 32;                 // points per sub-batch
     static constexpr int KS = P / 16;            // k-steps per sub-batch
+    static constexpr int FLUSH_SB = 4;           // sub-batches per register -> shared flush (128 points)
     static constexpr int NT = BT / 8;            // n8 tiles
     static constexpr int CAP = P + NTHR;
     static constexpr int RS = BT + 8;            // outer row stride (floats): conflict-free float2 flush
@@ -148,6 +149,42 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
         const float xmax = (float)(xn - 1), ymax = (float)(yn - 1);
         const int Tlo = tT0, Thi = tT0 + gt1 - 1;
 
+        // MMA accumulators live across FLUSH_SB sub-batches; then they are added
+        // into the shared tile accumulator [y*16+x][t] (two-level summation).
+        float cacc[2][K::NT][4];
+        auto zero_acc = [&]() {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < K::NT; ++nt)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) cacc[mt][nt][j] = 0.f;
+        };
+        int pending = 0;
+        auto flush = [&]() {
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt) {
+                const int y = 2 * warp + mt;
+#pragma unroll
+                for (int nt = 0; nt < K::NT; ++nt) {
+                    float2 *o0 = reinterpret_cast<float2 *>(&outer[(y * 16 + gq) * K::RS + 8 * nt + 2 * tq]);
+                    float2 *o1 = reinterpret_cast<float2 *>(&outer[(y * 16 + gq + 8) * K::RS + 8 * nt + 2 * tq]);
+                    float2 v0 = make_float2(cacc[mt][nt][0], cacc[mt][nt][1]);
+                    float2 v1 = make_float2(cacc[mt][nt][2], cacc[mt][nt][3]);
+                    if (touched) {       // first flush writes, later ones add
+                        const float2 u0 = *o0, u1 = *o1;
+                        v0.x += u0.x; v0.y += u0.y;
+                        v1.x += u1.x; v1.y += u1.y;
+                    }
+                    *o0 = v0;
+                    *o1 = v1;
+                }
+            }
+            touched = true;
+            pending = 0;
+            zero_acc();
+        };
+        zero_acc();
         int head = 0, tail = 0;
         for (int cb = cbeg; cb < cend; cb += K::NTHR) {
             const int i = cb + tid;
@@ -234,7 +271,7 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                     float u = fabsf((float)xx - bpx[p]) * g.inv_rs;
                     float av;
                     if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - u; av = a * a; }
-                    else av = 1.0f - u * u;
+                    else av = MMA_SCALE * (1.0f - u * u);        // additive form: both terms scaled
                     axT[xx * K::AXS + p] = (p < np) ? av : 0.f;
                 }
                 for (int e = tid; e < 16 * K::P; e += K::NTHR) {           // a_y and the chord, [y][p]
@@ -243,21 +280,15 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                     uint32_t m = 0u;
                     if (p < np) {
                         float v = fabsf((float)yy - bpy[p]) * g.inv_rs;
-                        if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - v; ay = a * a; }
-                        else ay = -(v * v);
+                        // a_y carries the 2^15 FP16-range scale of the S operand
+                        if (KK == STKDE_KERNEL_PRINTED) { float a = 1.0f - v; ay = MMA_SCALE * (a * a); }
+                        else ay = -MMA_SCALE * (v * v);
                         if (yy < yn && v < 1.0f + CULL_BAND) m = row_mask16(g, brec[p], tX0, tY0 + yy);
                     }
                     rowT[e] = make_float2(ay, __uint_as_float(m));
                 }
                 __syncthreads();
                 // ---------------- tensor-core accumulation ----------------
-                float cacc[2][K::NT][4];
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-                    for (int nt = 0; nt < K::NT; ++nt)
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) cacc[mt][nt][j] = 0.f;
 #pragma unroll
                 for (int ks = 0; ks < K::KS; ++ks) {
                     const int ntm = __reduce_or_sync(0xffffffffu, lane < 16 ? meta[16 * ks + lane] : 0);
@@ -285,28 +316,21 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                         const float2 aG01 = *reinterpret_cast<const float2 *>(&axT[(gq + 8) * K::AXS + 16 * ks + 2 * tq]);
                         const float2 aG89 = *reinterpret_cast<const float2 *>(&axT[(gq + 8) * K::AXS + 16 * ks + 2 * tq + 8]);
                         const uint32_t bg = 1u << gq, bG = 1u << (gq + 8);
+                        // s = mask ? K_s (scaled, > 0 inside the disc, clamped to the
+                        // smallest normal FP16) : 0
+                        auto ks_ = [](float a, float b) {
+                            return KK == STKDE_KERNEL_PRINTED ? a * b : a + b;
+                        };
+                        constexpr float TINY = 6.103515625e-05f;
                         float s[8];
-                        if (KK == STKDE_KERNEL_PRINTED) {
-                            s[0] = (m0 & bg) ? ag01.x * r01.x : 0.f;   // row x=g,   k=2t
-                            s[1] = (m1 & bg) ? ag01.y * r01.z : 0.f;   // row x=g,   k=2t+1
-                            s[2] = (m0 & bG) ? aG01.x * r01.x : 0.f;   // row x=g+8, k=2t
-                            s[3] = (m1 & bG) ? aG01.y * r01.z : 0.f;
-                            s[4] = (m8 & bg) ? ag89.x * r89.x : 0.f;   // row x=g,   k=2t+8
-                            s[5] = (m9 & bg) ? ag89.y * r89.z : 0.f;
-                            s[6] = (m8 & bG) ? aG89.x * r89.x : 0.f;   // row x=g+8, k=2t+8
-                            s[7] = (m9 & bG) ? aG89.y * r89.z : 0.f;
-                        } else {
-                            s[0] = (m0 & bg) ? ag01.x + r01.x : 0.f;
-                            s[1] = (m1 & bg) ? ag01.y + r01.z : 0.f;
-                            s[2] = (m0 & bG) ? aG01.x + r01.x : 0.f;
-                            s[3] = (m1 & bG) ? aG01.y + r01.z : 0.f;
-                            s[4] = (m8 & bg) ? ag89.x + r89.x : 0.f;
-                            s[5] = (m9 & bg) ? ag89.y + r89.z : 0.f;
-                            s[6] = (m8 & bG) ? aG89.x + r89.x : 0.f;
-                            s[7] = (m9 & bG) ? aG89.y + r89.z : 0.f;
-                        }
-#pragma unroll
-                        for (int j = 0; j < 8; ++j) s[j] = fp16_range(s[j]);
+                        s[0] = (m0 & bg) ? fmaxf(ks_(ag01.x, r01.x), TINY) : 0.f;   // row x=g,   k=2t
+                        s[1] = (m1 & bg) ? fmaxf(ks_(ag01.y, r01.z), TINY) : 0.f;   // row x=g,   k=2t+1
+                        s[2] = (m0 & bG) ? fmaxf(ks_(aG01.x, r01.x), TINY) : 0.f;   // row x=g+8, k=2t
+                        s[3] = (m1 & bG) ? fmaxf(ks_(aG01.y, r01.z), TINY) : 0.f;
+                        s[4] = (m8 & bg) ? fmaxf(ks_(ag89.x, r89.x), TINY) : 0.f;   // row x=g,   k=2t+8
+                        s[5] = (m9 & bg) ? fmaxf(ks_(ag89.y, r89.z), TINY) : 0.f;
+                        s[6] = (m8 & bG) ? fmaxf(ks_(aG89.x, r89.x), TINY) : 0.f;   // row x=g+8, k=2t+8
+                        s[7] = (m9 & bG) ? fmaxf(ks_(aG89.y, r89.z), TINY) : 0.f;
                         split2(s[0], s[1], ahi[mt][0], alo[mt][0]);
                         split2(s[2], s[3], ahi[mt][1], alo[mt][1]);
                         split2(s[4], s[5], ahi[mt][2], alo[mt][2]);
@@ -325,29 +349,14 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
                         }
                     }
                 }
-                // two-level summation: fragments -> shared tile accumulator [y*16+x][t]
-#pragma unroll
-                for (int mt = 0; mt < 2; ++mt) {
-                    const int y = 2 * warp + mt;
-#pragma unroll
-                    for (int nt = 0; nt < K::NT; ++nt) {
-                        float2 *o0 = reinterpret_cast<float2 *>(&outer[(y * 16 + gq) * K::RS + 8 * nt + 2 * tq]);
-                        float2 *o1 = reinterpret_cast<float2 *>(&outer[(y * 16 + gq + 8) * K::RS + 8 * nt + 2 * tq]);
-                        float2 v0 = make_float2(cacc[mt][nt][0], cacc[mt][nt][1]);
-                        float2 v1 = make_float2(cacc[mt][nt][2], cacc[mt][nt][3]);
-                        if (touched) {       // first sub-batch writes, later ones add
-                            const float2 u0 = *o0, u1 = *o1;
-                            v0.x += u0.x; v0.y += u0.y;
-                            v1.x += u1.x; v1.y += u1.y;
-                        }
-                        *o0 = v0;
-                        *o1 = v1;
-                    }
-                }
-                touched = true;
+                if (++pending == K::FLUSH_SB) flush();
                 head += np;
                 __syncthreads();
             }
+        }
+        if (pending) {
+            flush();
+            __syncthreads();
         }
 
         // ---------------- store: every voxel exactly once ----------------
