@@ -61,10 +61,14 @@ enum {
 };
 
 /* Tile-kernel engine (environment variable STKDE_ENGINE at plan creation;
- * default TENSOR).  SIMT: FP32 FFMA2 accumulation in registers.  TENSOR: the
- * per-tile contraction on tensor cores (mma.sync m16n8k16, FP16 3-term split,
- * FP32 accumulation) -- DESIGN.md §3.5. */
-enum { STKDE_ENGINE_SIMT = 0, STKDE_ENGINE_TENSOR = 1 };
+ * default TC).  SIMT: FP32 FFMA2 accumulation in registers (16x16 columns).
+ * TENSOR: the per-tile contraction on the legacy tensor-core path (mma.sync
+ * m16n8k16, FP16 3-term split, FP32 accumulation; 16x16 columns) -- DESIGN.md
+ * §3.5.  TC: the same contraction on 5th-generation tensor cores (tcgen05.mma
+ * kind::f16, M = 128 columns of a 16x8-column tile, A generated into TMEM,
+ * accumulator in TMEM) -- DESIGN.md §3.6.  All engines compute the same sums
+ * within the parity tolerance; they differ in speed only. */
+enum { STKDE_ENGINE_SIMT = 0, STKDE_ENGINE_TENSOR = 1, STKDE_ENGINE_TC = 2 };
 
 typedef struct stkde_plan_s *stkde_plan_t;
 

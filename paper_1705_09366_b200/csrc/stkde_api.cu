@@ -90,44 +90,68 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     g.inv_rt = (float)(tres / ht);
     g.Gx = (int)Gx; g.Gy = (int)Gy; g.Gt = (int)Gt;
     g.Hs = (int)Hs_d; g.Ht = (int)Ht_d;
-    // Tile height from the temporal window 2H_t+1.
-    int BT = g.Ht >= 16 ? 64 : (g.Ht >= 6 ? 32 : 16);
+    p->engine = env_int("STKDE_ENGINE", STKDE_ENGINE_TC);
+    if (p->engine != STKDE_ENGINE_SIMT && p->engine != STKDE_ENGINE_TENSOR && p->engine != STKDE_ENGINE_TC) {
+        set_error("bad STKDE_ENGINE"); free(p); return STKDE_EINVAL;
+    }
+    // the tcgen05 engine stores per-point chords as int8 offsets: H_s <= 120
+    if (p->engine == STKDE_ENGINE_TC && g.Hs > 120) p->engine = STKDE_ENGINE_TENSOR;
+    // Tile shape (DESIGN.md §3.4/§3.6): SIMT and mma.sync engines 16x16 columns x Bt
+    // from the temporal window 2H_t+1; tcgen05 engine 16x8 columns (UMMA M = 128)
+    // x Bt in {64, 128} (the accumulator lives in 128 of the CTA's 256 TMEM columns).
+    int BT, BYv;
+    if (p->engine == STKDE_ENGINE_TC) {
+        BYv = 8;
+        BT = Gt <= 64 ? 64 : 128;
+    } else {
+        BYv = BYW;
+        BT = g.Ht >= 16 ? 64 : (g.Ht >= 6 ? 32 : 16);
+    }
     BT = env_int("STKDE_BT", BT);
     int CT = BT >= 64 ? 16 : 8;
     CT = env_int("STKDE_CT", CT);
-    if (tile_smem_bytes(BT, CT) == 0) { set_error("unsupported tile shape Bt=%d CT=%d", BT, CT); free(p); return STKDE_EINVAL; }
+    if (p->engine == STKDE_ENGINE_TC ? tile_tc_smem_bytes(BT) == 0 : tile_smem_bytes(BT, CT) == 0) {
+        set_error("unsupported tile shape Bt=%d CT=%d for engine %d", BT, CT, p->engine); free(p); return STKDE_EINVAL;
+    }
     g.BT = BT;
+    g.BY = BYv;
     p->CT = CT;
     p->kernel = kernel_kind;
     g.kernel = kernel_kind;
     p->tile_threads = tile_threads(BT, CT);
     g.NTX = (int)((Gx + BX - 1) / BX);
-    g.NTY = (int)((Gy + BY - 1) / BY);
+    g.NTY = (int)((Gy + BYv - 1) / BYv);
     g.NTT = (int)((Gt + BT - 1) / BT);
     g.Ra = (g.Hs + BX - 1) / BX;
+    g.Ray = (g.Hs + BYv - 1) / BYv;
     g.Rt = (g.Ht + BT - 1) / BT;
     p->ntiles = (int64_t)g.NTX * g.NTY * g.NTT;
     if (p->ntiles >= ((int64_t)1 << 30)) { set_error("grid has too many tiles"); free(p); return STKDE_EINVAL; }
-    const int64_t nseg_max = (int64_t)std::min(2 * g.Ra + 1, g.NTY) * std::min(2 * g.Rt + 1, g.NTT);
+    const int64_t nseg_max = (int64_t)std::min(2 * g.Ray + 1, g.NTY) * std::min(2 * g.Rt + 1, g.NTT);
     if (nseg_max > MAXSEG) { set_error("bandwidth too large for the tile shape (%lld segments)", (long long)nseg_max); free(p); return STKDE_EINVAL; }
     p->max_n = max_n;
     p->key_bits = key_bits_for(p->ntiles);
 
     // Work-item and split-slot bounds: total candidates <= n * buckets per tile.
-    const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ra + 1, g.NTY) *
+    const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ray + 1, g.NTY) *
                        std::min(2 * g.Rt + 1, g.NTT);
     const int64_t cand_bound = std::max<int64_t>(max_n, 1) * nb;
-    const size_t tile_bytes = (size_t)256 * BT * 4;
+    const size_t tile_bytes = (size_t)(p->engine == STKDE_ENGINE_TC ? 128 : 256) * BT * 4;
     const int64_t slot_budget = (int64_t)env_int("STKDE_SLOT_MB", 1024) * (1 << 20) / (int64_t)tile_bytes;
     int64_t chunk = std::max<int64_t>(env_int("STKDE_CHUNK", 4096), (2 * cand_bound + slot_budget - 1) / slot_budget);
+    // tcgen05 engine: the S32 accumulators take <= 129796 per point,
+    // so a work item may accumulate at most 16545 points before 2^31.
+    if (p->engine == STKDE_ENGINE_TC) chunk = std::min<int64_t>(chunk, 16384);
     chunk = std::min<int64_t>(chunk, (int64_t)1 << 30);
     p->chunk = (int)chunk;
     p->max_items = p->ntiles + cand_bound / chunk + 1;
     p->max_slots = 2 * (cand_bound / chunk) + 2;
-    p->engine = env_int("STKDE_ENGINE", STKDE_ENGINE_TENSOR);
-    if (p->engine != STKDE_ENGINE_SIMT && p->engine != STKDE_ENGINE_TENSOR) { set_error("bad STKDE_ENGINE"); free(p); return STKDE_EINVAL; }
     int rc;
-    if (p->engine == STKDE_ENGINE_TENSOR) {
+    if (p->engine == STKDE_ENGINE_TC) {
+        p->tile_threads = 256;
+        p->smem_bytes = tile_tc_smem_bytes(BT);
+        rc = tile_tc_occupancy(BT, kernel_kind, &p->ctas_per_sm);
+    } else if (p->engine == STKDE_ENGINE_TENSOR) {
         p->tile_threads = 256;
         p->smem_bytes = tile_mma_smem_bytes(BT);
         rc = tile_mma_occupancy(BT, kernel_kind, &p->ctas_per_sm);
@@ -156,6 +180,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     Part parts[] = {
         {(void **)&p->rec, nrec * sizeof(PointRec)},
         {(void **)&p->rec_sorted, nrec * sizeof(PointRec)},
+        {(void **)&p->chords, p->engine == STKDE_ENGINE_TC ? nrec * (size_t)(2 * g.Hs + 1) * 2 : 0},
         {(void **)&p->keys_in, nrec * 4}, {(void **)&p->keys_out, nrec * 4},
         {(void **)&p->vals_in, nrec * 4}, {(void **)&p->vals_out, nrec * 4},
         {(void **)&p->bucket_cnt, (nt + 1) * 4}, {(void **)&p->bucket_begin, (nt + 2) * 4},
@@ -235,11 +260,16 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
     const float cnorm = (float)(kc / ((double)n_norm * (g.hs * g.hs) * g.ht));
     int rc = launch_binning(p, d_points, n, st);
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    if (p->engine == STKDE_ENGINE_TC) {
+        rc = launch_chords(p, n, st);
+        if (rc) { set_error("chord launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    }
     const int c0 = (int)(t_begin / g.BT), c1 = (int)((t_end + g.BT - 1) / g.BT);
     rc = launch_worklist(p, c0, c1, st);
     if (rc) { set_error("work-list launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
-    rc = p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
-                                          : launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
+    rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
+         : p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
+                                            : launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
     if (rc) { set_error("tile kernel launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     return STKDE_OK;
 }
@@ -391,7 +421,7 @@ extern "C" int stkde_plan_check(stkde_plan_t p) {
 
 extern "C" int stkde_plan_info(stkde_plan_t p, stkde_plan_info_t *info) {
     if (!p || !info) { set_error("NULL argument"); return STKDE_EINVAL; }
-    info->Bx = BX; info->By = BY; info->Bt = p->g.BT;
+    info->Bx = BX; info->By = p->g.BY; info->Bt = p->g.BT;
     info->Hs = p->g.Hs; info->Ht = p->g.Ht;
     info->ntiles = p->ntiles;
     info->workspace_bytes = (int64_t)p->ws_bytes;

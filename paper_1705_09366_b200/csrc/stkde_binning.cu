@@ -63,7 +63,7 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
         r = PointRec{0, 0, 0, 0.f, 0.f, 0.f, 0.f, 0.f};
     } else if (reaches_grid(g, r)) {
         int a = min(max(r.X, 0), g.Gx - 1) / BX;
-        int b = min(max(r.Y, 0), g.Gy - 1) / BY;
+        int b = min(max(r.Y, 0), g.Gy - 1) / g.BY;
         int c = min(max(r.T, 0), g.Gt - 1) / g.BT;
         key = (uint32_t)((c * g.NTY + b) * g.NTX + a);
     }
@@ -80,11 +80,31 @@ __global__ void k_permute(const PointRec *__restrict__ rec, const uint32_t *__re
     if (j < n) out[j] = rec[vals[j]];
 }
 
+// Exact disc chords of every (sorted) point, for the tcgen05 engine: row
+// Y = Y_i - H_s + j (j = 0 .. 2H_s) holds the columns [X_i + lo, X_i + hi]
+// whose centres pass the spatial gate of Alg. 1, computed once
+// per point instead of once per (point, tile) visit; stored as int8 (lo, hi)
+// (lo > hi: empty row).  Requires H_s <= 120.
+__global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams g, uint16_t *__restrict__ chords) {
+    const int rows = 2 * g.Hs + 1;
+    const int64_t total = n * rows;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / rows;
+        const int j = (int)(e - i * rows);
+        const PointRec r = rec[i];
+        int lo, hi;
+        row_chord(g, r, r.Y - g.Hs + j, &lo, &hi);
+        int dl = lo - r.X, dh = hi - r.X;
+        if (dl > dh) { dl = 1; dh = 0; }
+        chords[e] = (uint16_t)((uint8_t)(int8_t)dl | ((uint16_t)(uint8_t)(int8_t)dh << 8));
+    }
+}
+
 // Candidate count of a tile: sum of its home-bucket segments.
 __device__ __forceinline__ uint32_t tile_candidates(const GridParams &g, const uint32_t *__restrict__ bb,
                                                     int a, int b, int c) {
     int a0 = max(a - g.Ra, 0), a1 = min(a + g.Ra, g.NTX - 1);
-    int b0 = max(b - g.Ra, 0), b1 = min(b + g.Ra, g.NTY - 1);
+    int b0 = max(b - g.Ray, 0), b1 = min(b + g.Ray, g.NTY - 1);
     int c0 = max(c - g.Rt, 0), c1 = min(c + g.Rt, g.NTT - 1);
     uint32_t s = 0;
     for (int cc = c0; cc <= c1; ++cc)
@@ -211,6 +231,16 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
         return STKDE_ECUDA;
     p->last_own_launches += 2;
     p->last_cub_calls += 2;
+    return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
+}
+
+int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
+    const int64_t total = n * (2 * p->g.Hs + 1);
+    if (total > 0) {
+        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 16);
+        k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords);
+        p->last_own_launches += 1;
+    }
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }
 

@@ -16,8 +16,8 @@
 
 namespace stkde {
 
-constexpr int BX = 16;            // tile width in X (voxels)
-constexpr int BY = 16;            // tile width in Y (voxels)
+constexpr int BX = 16;            // tile width in X (voxels), all engines
+constexpr int BYW = 16;           // tile width in Y of the SIMT / mma.sync engines (g.BY = 8 for tcgen05)
 constexpr int MAXSEG = 256;       // max home-bucket segments per tile
 // Relative band around the disc edge inside which the FP32 gate defers to
 // the exact FP64 expression (reading R13): |d^2 - r^2| <= BAND r^2.
@@ -48,8 +48,8 @@ struct GridParams {
     int Gx, Gy, Gt;         // grid (voxels)
     int Hs, Ht;             // ceil(hs/sres), ceil(ht/tres)
     int NTX, NTY, NTT;      // tiles per axis
-    int BT;                 // tile height (layers)
-    int Ra, Rt;             // home-bucket reach in tiles: ceil(Hs/BX), ceil(Ht/BT)
+    int BY, BT;             // tile width in Y (columns), tile height (layers)
+    int Ra, Ray, Rt;        // home-bucket reach in tiles: ceil(Hs/BX), ceil(Hs/BY), ceil(Ht/BT)
     int kernel;             // STKDE_KERNEL_*
 };
 
@@ -138,7 +138,7 @@ struct stkde_plan_s {
     stkde::GridParams g;
     int kernel;
     int CT;                   // layers per thread of the tile kernel (4 columns x CT)
-    int engine;               // STKDE_ENGINE_*: 0 = FP32 FFMA2 (SIMT), 1 = tensor-core mma.sync 3xFP16
+    int engine;               // STKDE_ENGINE_*: 0 = FP32 FFMA2 (SIMT), 1 = mma.sync 3xFP16, 2 = tcgen05 3xFP16
     int tile_threads;
     int ctas_per_sm;
     int64_t max_n;
@@ -153,6 +153,7 @@ struct stkde_plan_s {
     void *ws;
     size_t ws_bytes;
     stkde::PointRec *rec, *rec_sorted;
+    uint16_t *chords;           // tcgen05 engine: [max_n][2Hs+1] exact disc chords (int8 lo, hi - X_i)
     uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
     uint32_t *bucket_cnt;       // [ntiles + 1]
     uint32_t *bucket_begin;     // [ntiles + 2]
@@ -178,6 +179,7 @@ struct stkde_plan_s {
 namespace stkde {
 // launchers (stkde_binning.cu / stkde_tile.cu)
 int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
+int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st);
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,
                 float *out, cudaStream_t st);
@@ -193,5 +195,9 @@ size_t tile_mma_smem_bytes(int BT);
 int tile_mma_occupancy(int BT, int kernel, int *ctas_per_sm);
 int launch_tile_mma(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float cscale, float *out,
                     cudaStream_t st);
+size_t tile_tc_smem_bytes(int BT);
+int tile_tc_occupancy(int BT, int kernel, int *ctas_per_sm);
+int launch_tile_tc(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float cscale, float *out,
+                   cudaStream_t st);
 void set_error(const char *fmt, ...);
 }  // namespace stkde

@@ -117,15 +117,15 @@ k_tile_mma(const GridParams g, const PointRec *__restrict__ recs, const uint32_t
         const int4 item = items[it];
         const int ls = item.x, jchunk = item.y, nch = item.z;
         const int ta = ls % g.NTX, tb = (ls / g.NTX) % g.NTY, tc = ls / (g.NTX * g.NTY) + c0;
-        const int tX0 = ta * BX, tY0 = tb * BY, tT0 = tc * BT;
+        const int tX0 = ta * BX, tY0 = tb * BYW, tT0 = tc * BT;
         const int lt0 = max(0, (int)(t_begin - tT0));
         const int lt1 = min(BT, (int)min((int64_t)g.Gt, t_end) - tT0);
-        const int xn = min(BX, g.Gx - tX0), yn = min(BY, g.Gy - tY0);
+        const int xn = min(BX, g.Gx - tX0), yn = min(BYW, g.Gy - tY0);
         const int gt1 = min(BT, g.Gt - tT0);
 
         // ---- home-bucket segments of this tile ----
         const int a0 = max(ta - g.Ra, 0), a1 = min(ta + g.Ra, g.NTX - 1);
-        const int b0 = max(tb - g.Ra, 0), b1 = min(tb + g.Ra, g.NTY - 1);
+        const int b0 = max(tb - g.Ray, 0), b1 = min(tb + g.Ray, g.NTY - 1);
         const int cc0 = max(tc - g.Rt, 0), cc1 = min(tc + g.Rt, g.NTT - 1);
         const int nb = b1 - b0 + 1, nseg = nb * (cc1 - cc0 + 1);
         for (int k = tid; k < nseg; k += K::NTHR) {

@@ -73,7 +73,7 @@ def make_points(n, g, clustered, seed):
     return np.concatenate([p, extra]).astype(np.float32)
 
 
-@pytest.fixture(params=[1, 0], ids=["tensor", "simt"])
+@pytest.fixture(params=[2, 1, 0], ids=["tc", "mma", "simt"])
 def engine(request):
     old = os.environ.get("STKDE_ENGINE")
     os.environ["STKDE_ENGINE"] = str(request.param)
@@ -141,12 +141,14 @@ def test_determinism_and_slabs(S, engine):
         bt = p.info()["Bt"]
         assert torch.equal(a, b)
         # Bt-aligned and unaligned slabs equal the corresponding layers bitwise
-        for t0, t1 in [(0, bt), (bt, 3 * bt), (3, 50), (50, 51), (g["Gt"] - 5, g["Gt"])]:
+        Gt = g["Gt"]
+        for t0, t1 in [(0, min(bt, Gt)), (min(bt, Gt - 1), min(3 * bt, Gt)), (3, 50), (50, 51), (Gt - 5, Gt)]:
             s = p.compute_slab(t, t0, t1, n_norm=w.n)
             assert torch.equal(s, a[:, :, t0:t1]), (t0, t1)
-        cuts = p.slab_partition(t, 4)
+        nparts = min(4, (Gt + bt - 1) // bt)       # at most one part per Bt block
+        cuts = p.slab_partition(t, nparts)
         assert cuts[0] == 0 and cuts[-1] == g["Gt"] and all(c % bt == 0 for c in cuts[:-1])
-        assert all(cuts[i] < cuts[i + 1] for i in range(4))
+        assert all(cuts[i] < cuts[i + 1] for i in range(nparts))
 
 
 def test_split_hot_tiles(S, oracle_mod, engine):
@@ -178,6 +180,21 @@ def test_tile_variants(S, oracle_mod, bt_c):
     assert info["Bt"] == bt_c[0]
     ref = oracle_mod.stkde_pb(w.points, **g)
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=str(bt_c))
+
+
+@pytest.mark.parametrize("bt", [64, 128])
+def test_tc_tile_heights(S, oracle_mod, bt):
+    # tcgen05 engine at both tile heights on a grid where both are legal
+    w = synth.make_config("dengue")
+    g = w.grid_kwargs()
+    os.environ["STKDE_BT"], os.environ["STKDE_ENGINE"] = str(bt), "2"
+    try:
+        gpu, _, info = run_gpu(S, w.points, **g)
+    finally:
+        del os.environ["STKDE_BT"], os.environ["STKDE_ENGINE"]
+    assert info["Bt"] == bt and info["By"] == 8 and info["engine"] == 2
+    ref = oracle_mod.stkde_pb(w.points, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="tc bt=%d" % bt)
 
 
 def test_sharded_single_process_equals_full(S):

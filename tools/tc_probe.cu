@@ -1,0 +1,487 @@
+// tc_probe.cu -- standalone B200 probe of the tcgen05 conventions the STKDE
+// tensor engine relies on (development tool, not product code):
+//   1. A-from-TMEM FP16 packing, B K-major no-swizzle smem layout, D layout
+//   2. N-trimmed MMAs (D column offset + B row offset)
+//   3. accumulate chains over several A/B blocks
+//   4. issue rate of back-to-back TS MMAs at N = 16 ... 256
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 tools/tc_probe.cu -o tools/tc_probe
+#include <cuda_fp16.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../paper_1705_09366_b200/csrc/tc_ptx.cuh"
+
+using namespace stkde;
+
+constexpr int M = 128;
+constexpr int NMAX = 256;
+constexpr uint32_t LBO = 128, SBO = 256;
+
+// B[n][k] (N x 16) -> smem byte offset
+__host__ __device__ inline uint32_t boff(int n, int k) { return (n / 8) * SBO + (k / 8) * LBO + (n % 8) * 16 + (k % 8) * 2; }
+
+// mode 0: D[:, 0:256] = A0 . B0^T          (N = 256)
+// mode 1: D = 0 (N=256 with zero B) then D[:, off:off+nn] += A0 . B0[off:off+nn]^T
+// mode 2: D = A0.B0^T + A1.B1^T + A0.B1^T  (3-term chain, N = 256)
+__global__ void k_layout(const __half *A0, const __half *A1, const __half *B0, const __half *B1, float *D, int mode,
+                         int off, int nn) {
+    __shared__ __align__(1024) unsigned char sb[2][NMAX * 16 * 2];
+    __shared__ __align__(1024) unsigned char szero[NMAX * 16 * 2];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int e = tid; e < NMAX * 16; e += blockDim.x) {
+        int n = e / 16, k = e % 16;
+        *reinterpret_cast<__half *>(&sb[0][boff(n, k)]) = B0[e];
+        *reinterpret_cast<__half *>(&sb[1][boff(n, k)]) = B1[e];
+        *reinterpret_cast<__half *>(&szero[boff(n, k)]) = __float2half(0.f);
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase;
+    const uint32_t a0col = 256, a1col = 264;
+    // thread m writes row m of A0 and A1: 16 halves -> 8 columns each
+    {
+        const int m = tid;   // 128 threads, warp w -> lanes 32w..32w+31
+        uint32_t v[16];
+        for (int j = 0; j < 8; ++j) {
+            __half2 h0 = __halves2half2(A0[m * 16 + 2 * j], A0[m * 16 + 2 * j + 1]);
+            __half2 h1 = __halves2half2(A1[m * 16 + 2 * j], A1[m * 16 + 2 * j + 1]);
+            v[j] = *reinterpret_cast<uint32_t *>(&h0);
+            v[8 + j] = *reinterpret_cast<uint32_t *>(&h1);
+        }
+        tc::tmem_st16(tb + ((uint32_t)(32 * warp) << 16) + a0col, v);
+        tc::tmem_wait_st();
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+        const uint64_t b0 = tc::smem_desc(tc::smem_u32(sb[0]), LBO, SBO);
+        const uint64_t b1 = tc::smem_desc(tc::smem_u32(sb[1]), LBO, SBO);
+        const uint64_t bz = tc::smem_desc(tc::smem_u32(szero), LBO, SBO);
+        if (mode == 0) {
+            tc::mma_ts(tb, tb + a0col, b0, tc::idesc_f16(M, 256), 0);
+        } else if (mode == 1) {
+            tc::mma_ts(tb, tb + a0col, bz, tc::idesc_f16(M, 256), 0);
+            const uint64_t bo = tc::smem_desc(tc::smem_u32(sb[0]) + (off / 8) * SBO, LBO, SBO);
+            tc::mma_ts(tb + off, tb + a0col, bo, tc::idesc_f16(M, nn), 1);
+        } else {
+            tc::mma_ts(tb, tb + a0col, b0, tc::idesc_f16(M, 256), 0);
+            tc::mma_ts(tb, tb + a1col, b1, tc::idesc_f16(M, 256), 1);
+            tc::mma_ts(tb, tb + a0col, b1, tc::idesc_f16(M, 256), 1);
+        }
+        tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after();
+    {
+        const int m = tid;
+        for (int c = 0; c < 256; c += 16) {
+            uint32_t v[16];
+            tc::tmem_ld16(tb + ((uint32_t)(32 * warp) << 16) + c, v);
+            tc::tmem_wait_ld();
+            for (int j = 0; j < 16; ++j) D[m * 256 + c + j] = __uint_as_float(v[j]);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+// issue rate: nmma back-to-back MMAs of width N, rotating over nacc accumulators
+// (D columns [(i % nacc) * N, +N)); issued by warp 0 with an elected lane
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t pred = 0;
+    asm volatile("{\n\t.reg .pred P1;\n\telect.sync _|P1, 0xffffffff;\n\tselp.b32 %0, 1, 0, P1;\n\t}" : "+r"(pred));
+    return pred;
+}
+__global__ void k_rate(int N, int nmma, long long *cyc, int ss, int nacc) {
+    __shared__ __align__(1024) unsigned char sb[NMAX * 16 * 2];
+    __shared__ __align__(1024) unsigned char sa[M * 16 * 2];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int e = tid; e < NMAX * 16 * 2 / 4; e += blockDim.x) reinterpret_cast<uint32_t *>(sb)[e] = 0x3c003c00u;
+    for (int e = tid; e < M * 16 * 2 / 4; e += blockDim.x) reinterpret_cast<uint32_t *>(sa)[e] = 0x3c003c00u;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    tc::fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase;
+    if (warp == 0) {
+        const uint32_t id = tc::idesc_f16(M, N);
+        const uint64_t b = tc::smem_desc(tc::smem_u32(sb), LBO, SBO);
+        const uint64_t a = tc::smem_desc(tc::smem_u32(sa), LBO, SBO);
+        long long t0 = clock64();
+        const uint32_t leader = elect_one();
+        if (leader) {
+            const uint32_t d0 = tb, d1 = tb + (nacc > 1 ? N : 0), d2 = tb + (nacc > 2 ? 2 * N : 0),
+                           d3 = tb + (nacc > 2 ? 3 * N : (nacc > 1 ? N : 0));
+            const uint32_t at = tb + 448;
+            if (ss) {
+                tc::mma_ss(d0, a, b, id, 0); tc::mma_ss(d1, a, b, id, 0);
+                tc::mma_ss(d2, a, b, id, 0); tc::mma_ss(d3, a, b, id, 0);
+            } else {
+                tc::mma_ts(d0, at, b, id, 0); tc::mma_ts(d1, at, b, id, 0);
+                tc::mma_ts(d2, at, b, id, 0); tc::mma_ts(d3, at, b, id, 0);
+            }
+            for (int i = 4; i < nmma; i += 8) {
+                if (ss) {
+                    tc::mma_ss(d0, a, b, id, 1); tc::mma_ss(d1, a, b, id, 1);
+                    tc::mma_ss(d2, a, b, id, 1); tc::mma_ss(d3, a, b, id, 1);
+                    tc::mma_ss(d0, a, b, id, 1); tc::mma_ss(d1, a, b, id, 1);
+                    tc::mma_ss(d2, a, b, id, 1); tc::mma_ss(d3, a, b, id, 1);
+                } else {
+                    tc::mma_ts(d0, at, b, id, 1); tc::mma_ts(d1, at, b, id, 1);
+                    tc::mma_ts(d2, at, b, id, 1); tc::mma_ts(d3, at, b, id, 1);
+                    tc::mma_ts(d0, at, b, id, 1); tc::mma_ts(d1, at, b, id, 1);
+                    tc::mma_ts(d2, at, b, id, 1); tc::mma_ts(d3, at, b, id, 1);
+                }
+            }
+            tc::mma_commit(&bar);
+        }
+        __syncwarp();
+        tc::mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (tid == 0) cyc[0] = t1 - t0;
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+// accumulation rounding: D starts at 1.0 (via one MMA), then nacc MMAs each add
+// A.B = 16 * (2^-12 * 1.0) ... per element the exact sum is known; report bias
+__global__ void k_round(int nacc, float *res) {
+    __shared__ __align__(1024) unsigned char sb[64 * 16 * 2];
+    __shared__ __align__(1024) unsigned char sb1[64 * 16 * 2];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    // B (64 x 16): row n: value 2^-(n/4) * (1 + small) ... use fp16 values b_n = 1 + n/1024
+    for (int e = tid; e < 64 * 16; e += blockDim.x) {
+        int n = e / 16, k = e % 16;
+        *reinterpret_cast<__half *>(&sb[boff(n, k)]) = __float2half(k == 0 ? 1.0f : 0.0f);      // D := A[:,0]
+        *reinterpret_cast<__half *>(&sb1[boff(n, k)]) = __float2half(ldexpf(1.0f + (float)(n % 7) / 8.0f, -(n / 4) - 10));
+    }
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase;
+    {   // A: row m: k=0 -> 1.0 + m/256 ; k>0 -> 1.0 + ((m*k) % 13)/16
+        const int m = tid;
+        uint32_t v[8];
+        for (int j = 0; j < 8; ++j) {
+            float a0 = (2 * j == 0) ? 1.0f + (float)m / 256.0f : 1.0f + (float)((m * (2 * j)) % 13) / 16.0f;
+            float a1 = 1.0f + (float)((m * (2 * j + 1)) % 13) / 16.0f;
+            __half2 h = __floats2half2_rn(a0, a1);
+            v[j] = *reinterpret_cast<uint32_t *>(&h);
+        }
+        tc::tmem_st8(tb + ((uint32_t)(32 * warp) << 16) + 256, v);
+        tc::tmem_wait_st();
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+        const uint64_t b0 = tc::smem_desc(tc::smem_u32(sb), LBO, SBO), b1 = tc::smem_desc(tc::smem_u32(sb1), LBO, SBO);
+        tc::mma_ts(tb, tb + 256, b0, tc::idesc_f16(M, 64), 0);
+        for (int i = 0; i < nacc; ++i) tc::mma_ts(tb, tb + 256, b1, tc::idesc_f16(M, 64), 1);
+        tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after();
+    {
+        const int m = tid;
+        for (int c = 0; c < 64; c += 16) {
+            uint32_t v[16];
+            tc::tmem_ld16(tb + ((uint32_t)(32 * warp) << 16) + c, v);
+            tc::tmem_wait_ld();
+            for (int j = 0; j < 16; ++j) res[m * 64 + c + j] = __uint_as_float(v[j]);
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+// TMEM load throughput: nw warps (multiple of 4), each loads its quarter's 32 lanes x ncols, reps times
+__global__ void k_ldtm(int ncols, int reps, long long *cyc, float *sink) {
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase + ((uint32_t)(32 * (warp & 3)) << 16);
+    const int nw = blockDim.x / 32, part = warp >> 2, nparts = nw / 4;
+    float acc = 0.f;
+    __syncthreads();
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+        for (int c = part * 16; c < ncols; c += 16 * nparts) {
+            uint32_t v[16];
+            tc::tmem_ld16(tb + c, v);
+            tc::tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc += __uint_as_float(v[j]);
+        }
+    }
+    __syncthreads();
+    long long t1 = clock64();
+    if (tid == 0) cyc[0] = t1 - t0;
+    sink[tid] = acc;
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tbase);
+}
+
+__host__ __device__ constexpr uint32_t idesc_u8(int Mm, int N) {
+    return (2u << 4)                      // D format S32
+           | (0u << 7) | (0u << 10)       // A, B unsigned 8-bit
+           | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(Mm >> 4) << 24);
+}
+__device__ __forceinline__ void mma_ts_i8(uint32_t d, uint32_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}"
+                 ::"r"(d), "r"(a), "l"(b), "r"(id), "r"(acc) : "memory");
+}
+// B[n][k] (N x 32 bytes) -> smem byte offset (K-major core matrices of 8 rows x 16 B)
+__host__ __device__ inline uint32_t boff8(int n, int k) { return (n / 8) * SBO + (k / 16) * LBO + (n % 8) * 16 + (k % 16); }
+
+// D[128 x 64] = A0 (u8 128x32, TMEM) . B0^T (u8 64x32, smem) ; then + A1.B0^T at cols [off, off+nn)
+__global__ void k_i8(const uint8_t *A0, const uint8_t *A1, const uint8_t *B0, int *D, int off, int nn) {
+    __shared__ __align__(1024) unsigned char sb[64 * 32];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int e = tid; e < 64 * 32; e += blockDim.x) sb[boff8(e / 32, e % 32)] = B0[e];
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase;
+    {
+        const int m = tid;
+        uint32_t v[16];
+        for (int j = 0; j < 8; ++j) {
+            v[j] = (uint32_t)A0[m * 32 + 4 * j] | ((uint32_t)A0[m * 32 + 4 * j + 1] << 8) |
+                   ((uint32_t)A0[m * 32 + 4 * j + 2] << 16) | ((uint32_t)A0[m * 32 + 4 * j + 3] << 24);
+            v[8 + j] = (uint32_t)A1[m * 32 + 4 * j] | ((uint32_t)A1[m * 32 + 4 * j + 1] << 8) |
+                       ((uint32_t)A1[m * 32 + 4 * j + 2] << 16) | ((uint32_t)A1[m * 32 + 4 * j + 3] << 24);
+        }
+        tc::tmem_st16(tb + ((uint32_t)(32 * warp) << 16) + 256, v);
+        tc::tmem_wait_st();
+    }
+    tc::fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (tid == 0) {
+        const uint64_t b0 = tc::smem_desc(tc::smem_u32(sb), LBO, SBO);
+        mma_ts_i8(tb, tb + 256, b0, idesc_u8(M, 64), 0);
+        const uint64_t bo = tc::smem_desc(tc::smem_u32(sb) + (off / 8) * SBO, LBO, SBO);
+        mma_ts_i8(tb + off, tb + 264, bo, idesc_u8(M, nn), 1);
+        tc::mma_commit(&bar);
+    }
+    tc::mbar_wait(&bar, 0);
+    tc::fence_after();
+    {
+        const int m = tid;
+        for (int c = 0; c < 64; c += 16) {
+            uint32_t v[16];
+            tc::tmem_ld16(tb + ((uint32_t)(32 * warp) << 16) + c, v);
+            tc::tmem_wait_ld();
+            for (int j = 0; j < 16; ++j) D[m * 64 + c + j] = (int)v[j];
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+__global__ void k_rate_i8(int N, int nmma, long long *cyc) {
+    __shared__ __align__(1024) unsigned char sb[256 * 32];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int e = tid; e < 256 * 32 / 4; e += blockDim.x) reinterpret_cast<uint32_t *>(sb)[e] = 0x01010101u;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    tc::fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase;
+    if (warp == 0) {
+        const uint32_t id = idesc_u8(M, N);
+        const uint64_t b = tc::smem_desc(tc::smem_u32(sb), LBO, SBO);
+        long long t0 = clock64();
+        if (elect_one()) {
+            const uint32_t at = tb + 448;
+            mma_ts_i8(tb, at, b, id, 0);
+            for (int i = 1; i < nmma; i += 4) {
+                mma_ts_i8(tb, at, b, id, 1); mma_ts_i8(tb, at, b, id, 1);
+                mma_ts_i8(tb, at, b, id, 1); mma_ts_i8(tb, at, b, id, 1);
+            }
+            tc::mma_commit(&bar);
+        }
+        __syncwarp();
+        tc::mbar_wait(&bar, 0);
+        long long t1 = clock64();
+        if (tid == 0) cyc[0] = t1 - t0;
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+static float frand(unsigned &s) { s = s * 1664525u + 1013904223u; return (float)((int)((s >> 16) % 5) - 2); }
+
+int main() {
+    const int NA = M * 16, NB = NMAX * 16;
+    std::vector<__half> A0(NA), A1(NA), B0(NB), B1(NB);
+    std::vector<float> a0(NA), a1(NA), b0(NB), b1(NB);
+    unsigned s = 12345;
+    for (int i = 0; i < NA; ++i) { a0[i] = frand(s); a1[i] = frand(s); A0[i] = __float2half(a0[i]); A1[i] = __float2half(a1[i]); }
+    for (int i = 0; i < NB; ++i) { b0[i] = frand(s); b1[i] = frand(s); B0[i] = __float2half(b0[i]); B1[i] = __float2half(b1[i]); }
+    __half *dA0, *dA1, *dB0, *dB1;
+    float *dD;
+    cudaMalloc(&dA0, NA * 2); cudaMalloc(&dA1, NA * 2); cudaMalloc(&dB0, NB * 2); cudaMalloc(&dB1, NB * 2);
+    cudaMalloc(&dD, M * 256 * 4);
+    cudaMemcpy(dA0, A0.data(), NA * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(dA1, A1.data(), NA * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB0, B0.data(), NB * 2, cudaMemcpyHostToDevice);
+    cudaMemcpy(dB1, B1.data(), NB * 2, cudaMemcpyHostToDevice);
+    std::vector<float> D(M * 256);
+    auto dot = [&](const std::vector<float> &A, const std::vector<float> &B, int m, int n) {
+        float r = 0; for (int k = 0; k < 16; ++k) r += A[m * 16 + k] * B[n * 16 + k]; return r; };
+    int fails = 0;
+    struct Case { int mode, off, nn; } cases[] = {{0, 0, 256}, {1, 16, 32}, {1, 8, 16}, {1, 40, 64}, {1, 0, 48}, {2, 0, 256}};
+    for (auto c : cases) {
+        cudaMemset(dD, 0xff, M * 256 * 4);
+        k_layout<<<1, 128>>>(dA0, dA1, dB0, dB1, dD, c.mode, c.off, c.nn);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { printf("mode %d: CUDA error %s\n", c.mode, cudaGetErrorString(e)); return 1; }
+        cudaMemcpy(D.data(), dD, M * 256 * 4, cudaMemcpyDeviceToHost);
+        int bad = 0;
+        for (int m = 0; m < M; ++m)
+            for (int n = 0; n < 256; ++n) {
+                float ref;
+                if (c.mode == 0) ref = dot(a0, b0, m, n);
+                else if (c.mode == 1) ref = (n >= c.off && n < c.off + c.nn) ? dot(a0, b0, m, n) : 0.f;
+                else ref = dot(a0, b0, m, n) + dot(a1, b1, m, n) + dot(a0, b1, m, n);
+                if (D[m * 256 + n] != ref) { if (bad < 5) printf("  mismatch mode %d off %d nn %d: D[%d][%d] = %g ref %g\n", c.mode, c.off, c.nn, m, n, D[m * 256 + n], ref); ++bad; }
+            }
+        printf("layout mode %d off %d nn %d: %s (%d bad)\n", c.mode, c.off, c.nn, bad ? "FAIL" : "ok", bad);
+        fails += bad != 0;
+    }
+    long long *dc, hc;
+    cudaMalloc(&dc, 8);
+    for (int ss = 0; ss < 2; ++ss)
+        for (int nacc : {1, 2, 4})
+            for (int N : {16, 32, 64, 96, 128, 256}) {
+                if (N * nacc > 448) continue;
+                const int nm = 2052;
+                k_rate<<<1, 128>>>(N, nm, dc, ss, nacc);
+                k_rate<<<1, 128>>>(N, nm, dc, ss, nacc);
+                cudaError_t e = cudaDeviceSynchronize();
+                if (e != cudaSuccess) { printf("rate: CUDA error %s\n", cudaGetErrorString(e)); return 1; }
+                cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+                printf("%s nacc=%d N=%3d: %.2f cycles per MMA (floor N/2 = %d)\n", ss ? "SS" : "TS", nacc, N, (double)hc / nm, N / 2);
+            }
+    {   // accumulation rounding
+        float *dr;
+        cudaMalloc(&dr, M * 64 * 4);
+        std::vector<float> r(M * 64);
+        for (int nacc : {1, 16, 256, 2048}) {
+            k_round<<<1, 128>>>(nacc, dr);
+            if (cudaDeviceSynchronize() != cudaSuccess) { printf("round: error\n"); return 1; }
+            cudaMemcpy(r.data(), dr, M * 64 * 4, cudaMemcpyDeviceToHost);
+            double sumrel = 0, maxrel = 0;
+            for (int m = 0; m < M; ++m)
+                for (int n = 0; n < 64; ++n) {
+                    // exact: D = a0(m) * 1 + nacc * sum_k A[m][k] * b1(n)   (fp16 values are exact here)
+                    double a0 = (double)__half2float(__float2half(1.0f + (float)m / 256.0f));
+                    double sa = 0;
+                    for (int k = 0; k < 16; ++k) {
+                        float av = (k == 0) ? 1.0f + (float)m / 256.0f : 1.0f + (float)((m * k) % 13) / 16.0f;
+                        sa += (double)__half2float(__float2half(av));
+                    }
+                    double b = (double)__half2float(__float2half(ldexpf(1.0f + (float)(n % 7) / 8.0f, -(n / 4) - 10)));
+                    double ex = a0 + (double)nacc * sa * b;
+                    double rel = ((double)r[m * 64 + n] - ex) / ex;
+                    sumrel += rel; maxrel = fmax(maxrel, fabs(rel));
+                }
+            printf("accumulate nacc=%4d: mean rel err %.3e, max |rel| %.3e (fp32 ulp 1.19e-07)\n", nacc, sumrel / (M * 64), maxrel);
+        }
+    }
+    {   // LDTM throughput
+        float *sink;
+        cudaMalloc(&sink, 1024 * 4);
+        for (int nw : {4, 8, 16})
+            for (int ncols : {128, 512}) {
+                const int reps = 64;
+                k_ldtm<<<1, 32 * nw>>>(ncols, reps, dc, sink);
+                k_ldtm<<<1, 32 * nw>>>(ncols, reps, dc, sink);
+                if (cudaDeviceSynchronize() != cudaSuccess) { printf("ldtm: error\n"); return 1; }
+                cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+                double bytes = (double)reps * ncols * 128 * 4;
+                printf("LDTM %2d warps, %3d cols: %.1f B/cycle\n", nw, ncols, bytes / (double)hc);
+            }
+    }
+    {   // kind::i8 layout + rate
+        std::vector<uint8_t> a0(M * 32), a1(M * 32), b0(64 * 32);
+        unsigned ss = 777;
+        for (auto &v : a0) { ss = ss * 1664525u + 1013904223u; v = (uint8_t)(ss >> 24); }
+        for (auto &v : a1) { ss = ss * 1664525u + 1013904223u; v = (uint8_t)(ss >> 24); }
+        for (auto &v : b0) { ss = ss * 1664525u + 1013904223u; v = (uint8_t)(ss >> 24); }
+        uint8_t *da0, *da1, *db0; int *dd;
+        cudaMalloc(&da0, M * 32); cudaMalloc(&da1, M * 32); cudaMalloc(&db0, 64 * 32); cudaMalloc(&dd, M * 64 * 4);
+        cudaMemcpy(da0, a0.data(), M * 32, cudaMemcpyHostToDevice);
+        cudaMemcpy(da1, a1.data(), M * 32, cudaMemcpyHostToDevice);
+        cudaMemcpy(db0, b0.data(), 64 * 32, cudaMemcpyHostToDevice);
+        struct C8 { int off, nn; } c8[] = {{16, 32}, {0, 64}, {48, 16}};
+        for (auto c : c8) {
+            k_i8<<<1, 128>>>(da0, da1, db0, dd, c.off, c.nn);
+            if (cudaDeviceSynchronize() != cudaSuccess) { printf("i8: CUDA error\n"); return 1; }
+            std::vector<int> D(M * 64);
+            cudaMemcpy(D.data(), dd, M * 64 * 4, cudaMemcpyDeviceToHost);
+            int bad = 0;
+            for (int m = 0; m < M; ++m)
+                for (int n = 0; n < 64; ++n) {
+                    long long r = 0;
+                    for (int k = 0; k < 32; ++k) r += (long long)a0[m * 32 + k] * b0[n * 32 + k];
+                    if (n >= c.off && n < c.off + c.nn)
+                        for (int k = 0; k < 32; ++k) r += (long long)a1[m * 32 + k] * b0[n * 32 + k];
+                    if (D[m * 64 + n] != r) { if (bad < 3) printf("  i8 mismatch D[%d][%d]=%d ref %lld\n", m, n, D[m * 64 + n], r); ++bad; }
+                }
+            printf("i8 layout off %d nn %d: %s (%d bad)\n", c.off, c.nn, bad ? "FAIL" : "ok", bad);
+            fails += bad != 0;
+        }
+        for (int N : {16, 32, 64, 128, 256}) {
+            const int nm = 2049;
+            k_rate_i8<<<1, 128>>>(N, nm, dc);
+            k_rate_i8<<<1, 128>>>(N, nm, dc);
+            if (cudaDeviceSynchronize() != cudaSuccess) { printf("i8 rate: error\n"); return 1; }
+            cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+            printf("i8 TS N=%3d: %.2f cycles per MMA (K=32)\n", N, (double)hc / nm);
+        }
+    }
+    printf(fails ? "PROBE FAIL\n" : "PROBE OK\n");
+    return fails != 0;
+}
