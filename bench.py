@@ -39,6 +39,8 @@ import stkde_synth as synth  # noqa: E402
 METRIC = "point-voxel contributions/sec"
 UNIT = "contributions/s"
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x 2 x max SM clock
+ENGINES = {0: "SIMT FP32 FFMA2", 1: "mma.sync m16n8k16 3xFP16", 2: "tcgen05.mma kind::i8, exact S32"}
+KERNELS = {0: "stkde::k_tile<Bt=%d>", 1: "stkde::k_tile_mma<Bt=%d>", 2: "stkde::k_tile_tc<Bt=%d>"}
 CONFIG_INDEX = {"tiny": 0, "dengue": 1, "social": 2, "ornith": 3, "stress": 4}
 # oracle sample sizes for the cpu_baseline / reference legs (about 10-30 s of host work)
 ORACLE_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 600000, "ornith": 1000000, "stress": 150000}
@@ -47,14 +49,19 @@ REF_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 200000, "ornith": 200000,
 
 
 def peaks():
+    """(HBM GB/s, source), (dense bf16 TFLOP/s burst, source) from MEASURED_PEAKS.json, else the
+    B200_PROFILING.md fallbacks."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     hbm, src = 6650.0, "fallback (B200_PROFILING.md)"
+    bf16, bsrc = 1590.0, "fallback (B200_PROFILING.md)"
     if os.path.exists(p):
         try:
-            hbm, src = float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+            d = json.load(open(p))
+            hbm, src = float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+            bf16, bsrc = float(d["bf16_tflops"]), "measured (MEASURED_PEAKS.json, burst)"
         except Exception:
             pass
-    return hbm, src
+    return (hbm, src), (bf16, bsrc)
 
 
 def host_cores():
@@ -210,6 +217,7 @@ def gpu_main(args, w, rank, world, local_rank):
     own = plan.info()["last_own_launches"]
     cub = plan.info()["last_cub_calls"]
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    plan.mma_stats()                            # reset the issued-MMA counters (tcgen05 engine)
     plan.enable_kernel_timing(True)
     gpu_idx = local_rank
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -227,6 +235,7 @@ def gpu_main(args, w, rank, world, local_rank):
     ms_steps = [a.elapsed_time(b) for a, b in ev]
     kms, klaunch = plan.kernel_ms()
     plan.enable_kernel_timing(False)
+    mma_cols, mma_kblocks = plan.mma_stats()
     ms = sum(ms_steps) / len(ms_steps)
     kernel_ms = kms / max(klaunch, 1)
     vals = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
@@ -257,7 +266,7 @@ def gpu_main(args, w, rank, world, local_rank):
     d2h = w.G[0] * w.G[1] * w.G[2] * 4
 
     # ---- roofline of the dominant kernel (the tile kernel) ----
-    hbm_peak, hbm_src = peaks()
+    (hbm_peak, hbm_src), (bf16_peak, bf16_src) = peaks()
     grid_bytes = w.G[0] * w.G[1] * (t1 - t0) * 4
     t_fp32 = 2.0 * C / (FP32_NOMINAL_TFLOPS * 1e12)
     t_hbm = grid_bytes / (hbm_peak * 1e9)
@@ -271,11 +280,25 @@ def gpu_main(args, w, rank, world, local_rank):
         ach = grid_bytes / (kernel_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                 "peak_source": hbm_src}
-    roof["traffic"] = profile_traffic(w.name)
-    roof["kernel"] = "stkde::k_tile<Bt=%d,CT=%d>" % (info["Bt"], info["tile_layers_per_thread"])
+    roof["traffic"] = profile_traffic(w.name, info["engine"])
+    roof["kernel"] = KERNELS[info["engine"]] % info["Bt"]
     roof["kernel_ms"] = kernel_ms_max
     roof["algorithmic"] = {"flops": 2 * C, "bytes": grid_bytes,
                            "per_unit": "2 FLOP per contribution (one FMA acc += K_s*K_t), 4 B per voxel written once"}
+    # the tensor pipe's own roofline (tcgen05 engine): int8 ops the kernel issued per launch
+    # (7 MMAs of 128 x N x 32 per k-block, 2 ops per MAC) against the dense int8 peak
+    # = 2 x the measured dense bf16 peak (the guide's nominal int8:bf16 ratio on sm_100)
+    roof_tc = None
+    if info["engine"] == 2 and mma_kblocks > 0:
+        ops = 7 * 2 * 128 * 32 * mma_cols / args.steps
+        ach_t = ops / (kernel_ms * 1e-3) / 1e12
+        roof_tc = {"bound": "tensor", "achieved": ach_t, "peak": 2 * bf16_peak, "unit": "TOPS (int8)",
+                   "frac": ach_t / (2 * bf16_peak), "peak_source": "2 x " + bf16_src,
+                   "kblocks_per_launch": mma_kblocks / args.steps,
+                   "mean_mma_n": mma_cols / mma_kblocks,
+                   # contributions / (128 x N x 32 products per k-block): the share of the
+                   # tile contraction that is inside some disc and window
+                   "useful_fraction": C / (128 * 32 * mma_cols / args.steps)}
 
     result = None
     if rank == 0:
@@ -300,6 +323,8 @@ def gpu_main(args, w, rank, world, local_rank):
             "library_launches": {"cub_calls": cub * args.steps},
             "clocks": clk.summary(),
             "roofline": roof,
+            "roofline_tensor": roof_tc,
+            "engine": ENGINES[info["engine"]],
             "cpu_baseline": cpu,
         }
         print(json.dumps(result))
@@ -309,11 +334,13 @@ def gpu_main(args, w, rank, world, local_rank):
     return 0
 
 
-def profile_traffic(name):
+def profile_traffic(name, engine):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the tile kernel from the
+    committed ncu --set full capture of this workload and engine (profiles/traffic.json)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get(name)
+            return json.load(open(p)).get("%s/engine%d" % (name, engine))
         except Exception:
             return None
     return None

@@ -169,6 +169,12 @@ int stkde_plan_info(stkde_plan_t plan, stkde_plan_info_t *info);
 int stkde_plan_enable_kernel_timing(stkde_plan_t plan, int enable);
 int stkde_plan_kernel_ms(stkde_plan_t plan, double *ms_total, int64_t *launches);
 
+/* Instrumentation of the tcgen05 engine: since the last call,
+ * the sum over issued k-blocks of the MMA width N (each k-block issues 7
+ * tcgen05.mma kind::i8 of 128 x N x 32) and the number of k-blocks; both are
+ * reset.  Synchronises the device.  Zero for the other engines. */
+int stkde_plan_mma_stats(stkde_plan_t plan, int64_t *mma_columns, int64_t *kblocks);
+
 /* Human-readable message for a return code / the last error of this thread. */
 const char *stkde_strerror(int code);
 const char *stkde_last_error(void);

@@ -462,6 +462,18 @@ extern "C" int stkde_plan_kernel_ms(stkde_plan_t p, double *ms_total, int64_t *l
     return STKDE_OK;
 }
 
+extern "C" int stkde_plan_mma_stats(stkde_plan_t p, int64_t *mma_columns, int64_t *kblocks) {
+    if (!p || !mma_columns || !kblocks) { set_error("NULL argument"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    CK(cudaDeviceSynchronize());
+    unsigned long long v[2] = {0ull, 0ull};
+    CK(cudaMemcpy(v, p->counters + 2, sizeof v, cudaMemcpyDeviceToHost));
+    CK(cudaMemset(p->counters + 2, 0, sizeof v));
+    *mma_columns = (int64_t)v[0];
+    *kblocks = (int64_t)v[1];
+    return STKDE_OK;
+}
+
 extern "C" const char *stkde_strerror(int code) {
     switch (code) {
         case STKDE_OK: return "ok";

@@ -162,7 +162,8 @@ struct stkde_plan_s {
     int4 *items;                // [max_items]
     uint32_t *arrive;           // [ntiles]
     float *partials;            // [max_slots][256*BT]
-    int *counters;              // [0] work counter, [1] error flag, [2..] spare
+    int *counters;              // [0] work counter, [1] error flag, [2..3] u64 issued MMA columns,
+                                // [4..5] u64 issued k-blocks (tcgen05 engine instrumentation)
     int *hist_t;                // [Gt + 1] slab-partition histogram
     void *cub_tmp;
     size_t cub_bytes;

@@ -23,7 +23,7 @@ KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
 EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_compute_slab",
            "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
-           "stkde_plan_kernel_ms", "stkde_strerror", "stkde_last_error")
+           "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_strerror", "stkde_last_error")
 
 
 class StkdeError(RuntimeError):
@@ -68,13 +68,15 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_info.argtypes = [P, ctypes.POINTER(PlanInfo)]
     L.stkde_plan_enable_kernel_timing.argtypes = [P, I32]
     L.stkde_plan_kernel_ms.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(I64)]
+    L.stkde_plan_mma_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
     L.stkde_last_error.restype = ctypes.c_char_p
     for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition", "stkde_slab_cuts",
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
-                 "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms"):
+                 "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
+                 "stkde_plan_mma_stats"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -208,6 +210,12 @@ class Plan:
         ms, k = ctypes.c_double(0), ctypes.c_int64(0)
         _check(load_library().stkde_plan_kernel_ms(self._h, ctypes.byref(ms), ctypes.byref(k)))
         return ms.value, k.value
+
+    def mma_stats(self):
+        """(sum of MMA widths N, k-blocks) issued by the tcgen05 engine since the last call."""
+        c, k = ctypes.c_int64(0), ctypes.c_int64(0)
+        _check(load_library().stkde_plan_mma_stats(self._h, ctypes.byref(c), ctypes.byref(k)))
+        return c.value, k.value
 
 
 def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs: Sequence[torch.Tensor],
