@@ -175,6 +175,13 @@ int stkde_plan_kernel_ms(stkde_plan_t plan, double *ms_total, int64_t *launches)
  * reset.  Synchronises the device.  Zero for the other engines. */
 int stkde_plan_mma_stats(stkde_plan_t plan, int64_t *mma_columns, int64_t *kblocks);
 
+/* Development diagnostics of the tcgen05 engine: with STKDE_TC_PROF=1 in the
+ * environment at plan creation, the tile kernel accumulates clock64 phase
+ * totals of one thread per role (generator teams: [0..10], loader: [16..23];
+ * layout in stkde_tile_tc.cu); this copies the 32 u64 counters to out32 and
+ * resets them.  Synchronises the device. */
+int stkde_plan_tc_profile(stkde_plan_t plan, uint64_t *out32);
+
 /* Human-readable message for a return code / the last error of this thread. */
 const char *stkde_strerror(int code);
 const char *stkde_last_error(void);

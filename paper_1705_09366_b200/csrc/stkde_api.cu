@@ -125,16 +125,24 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     g.Ra = (g.Hs + BX - 1) / BX;
     g.Ray = (g.Hs + BYv - 1) / BYv;
     g.Rt = (g.Ht + BT - 1) / BT;
+    // Home-bucket depth in T: the tcgen05 engine bins points into 16x8x32 (16 when
+    // H_t <= 8) blocks so a tile fetches only the blocks its temporal reach meets;
+    // the legacy engines bin by whole tiles.
+    g.BTH = p->engine == STKDE_ENGINE_TC ? (g.Ht <= 8 ? 16 : 32) : BT;
+    g.BTH = env_int("STKDE_BTH", g.BTH);
+    if (g.BTH < 1) { set_error("bad STKDE_BTH"); free(p); return STKDE_EINVAL; }
+    g.NTTH = (int)((Gt + g.BTH - 1) / g.BTH);
     p->ntiles = (int64_t)g.NTX * g.NTY * g.NTT;
-    if (p->ntiles >= ((int64_t)1 << 30)) { set_error("grid has too many tiles"); free(p); return STKDE_EINVAL; }
-    const int64_t nseg_max = (int64_t)std::min(2 * g.Ray + 1, g.NTY) * std::min(2 * g.Rt + 1, g.NTT);
+    p->nbuckets = (int64_t)g.NTX * g.NTY * g.NTTH;
+    if (p->ntiles >= ((int64_t)1 << 30) || p->nbuckets >= ((int64_t)1 << 30)) { set_error("grid has too many tiles"); free(p); return STKDE_EINVAL; }
+    const int64_t ncc_max = std::min<int64_t>((BT - 1 + 2 * (int64_t)g.Ht) / g.BTH + 2, g.NTTH);
+    const int64_t nseg_max = (int64_t)std::min(2 * g.Ray + 1, g.NTY) * ncc_max;
     if (nseg_max > MAXSEG) { set_error("bandwidth too large for the tile shape (%lld segments)", (long long)nseg_max); free(p); return STKDE_EINVAL; }
     p->max_n = max_n;
-    p->key_bits = key_bits_for(p->ntiles);
+    p->key_bits = key_bits_for(p->nbuckets);
 
     // Work-item and split-slot bounds: total candidates <= n * buckets per tile.
-    const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ray + 1, g.NTY) *
-                       std::min(2 * g.Rt + 1, g.NTT);
+    const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ray + 1, g.NTY) * ncc_max;
     const int64_t cand_bound = std::max<int64_t>(max_n, 1) * nb;
     const size_t tile_bytes = (size_t)(p->engine == STKDE_ENGINE_TC ? 128 : 256) * BT * 4;
     const int64_t slot_budget = (int64_t)env_int("STKDE_SLOT_MB", 1024) * (1 << 20) / (int64_t)tile_bytes;
@@ -167,7 +175,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     size_t b1 = 0, b2 = 0, b3 = 0, b4 = 0;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b1, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                        (uint32_t *)nullptr, nmax, 0, p->key_bits));
-    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)(p->ntiles + 1)));
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, b2, (uint32_t *)nullptr, (uint32_t *)nullptr, (int)(p->nbuckets + 1)));
     CK(cub::DeviceRadixSort::SortPairs(nullptr, b3, (uint32_t *)nullptr, (uint32_t *)nullptr, (uint32_t *)nullptr,
                                        (uint32_t *)nullptr, (int)p->ntiles, 0, 32));
     CK(cub::DeviceScan::ExclusiveSum(nullptr, b4, (uint64_t *)nullptr, (uint64_t *)nullptr, (int)(p->ntiles + 1)));
@@ -180,17 +188,17 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     Part parts[] = {
         {(void **)&p->rec, nrec * sizeof(PointRec)},
         {(void **)&p->rec_sorted, nrec * sizeof(PointRec)},
-        {(void **)&p->chords, p->engine == STKDE_ENGINE_TC ? nrec * (size_t)(2 * g.Hs + 1) * 2 : 0},
+        {(void **)&p->chords, p->engine == STKDE_ENGINE_TC ? nrec * (size_t)chord_rows(g.Hs) * 2 : 0},
         {(void **)&p->keys_in, nrec * 4}, {(void **)&p->keys_out, nrec * 4},
         {(void **)&p->vals_in, nrec * 4}, {(void **)&p->vals_out, nrec * 4},
-        {(void **)&p->bucket_cnt, (nt + 1) * 4}, {(void **)&p->bucket_begin, (nt + 2) * 4},
+        {(void **)&p->bucket_cnt, ((size_t)p->nbuckets + 1) * 4}, {(void **)&p->bucket_begin, ((size_t)p->nbuckets + 2) * 4},
         {(void **)&p->lpt_key_in, nt * 4}, {(void **)&p->lpt_key_out, nt * 4},
         {(void **)&p->lpt_val_in, nt * 4}, {(void **)&p->lpt_val_out, nt * 4},
         {(void **)&p->chunk_pack, (nt + 1) * 8}, {(void **)&p->chunk_off, (nt + 1) * 8},
         {(void **)&p->items, (size_t)p->max_items * 16},
         {(void **)&p->arrive, nt * 4},
         {(void **)&p->partials, (size_t)p->max_slots * tile_bytes},
-        {(void **)&p->counters, 64 * 4},
+        {(void **)&p->counters, 128 * 4},
         {(void **)&p->hist_t, ((size_t)Gt + 1) * 4},
         {(void **)&p->cub_tmp, p->cub_bytes},
     };
@@ -210,7 +218,8 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
         off += pt.bytes;
     }
     CK(cudaMemset(p->arrive, 0, nt * 4));
-    CK(cudaMemset(p->counters, 0, 64 * 4));
+    CK(cudaMemset(p->counters, 0, 128 * 4));
+    p->tc_profile = env_int("STKDE_TC_PROF", 0);
     *out = p;
     return STKDE_OK;
 }
@@ -471,6 +480,15 @@ extern "C" int stkde_plan_mma_stats(stkde_plan_t p, int64_t *mma_columns, int64_
     CK(cudaMemset(p->counters + 2, 0, sizeof v));
     *mma_columns = (int64_t)v[0];
     *kblocks = (int64_t)v[1];
+    return STKDE_OK;
+}
+
+extern "C" int stkde_plan_tc_profile(stkde_plan_t p, uint64_t *out32) {
+    if (!p || !out32) { set_error("NULL argument"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(out32, p->counters + 32, 32 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemset(p->counters + 32, 0, 32 * sizeof(uint64_t)));
     return STKDE_OK;
 }
 

@@ -64,7 +64,7 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
     } else if (reaches_grid(g, r)) {
         int a = min(max(r.X, 0), g.Gx - 1) / BX;
         int b = min(max(r.Y, 0), g.Gy - 1) / g.BY;
-        int c = min(max(r.T, 0), g.Gt - 1) / g.BT;
+        int c = min(max(r.T, 0), g.Gt - 1) / g.BTH;
         key = (uint32_t)((c * g.NTY + b) * g.NTX + a);
     }
     atomicAdd(&bucket_cnt[key], 1u);
@@ -80,22 +80,27 @@ __global__ void k_permute(const PointRec *__restrict__ rec, const uint32_t *__re
     if (j < n) out[j] = rec[vals[j]];
 }
 
-// Exact disc chords of every (sorted) point, for the tcgen05 engine: row
-// Y = Y_i - H_s + j (j = 0 .. 2H_s) holds the columns [X_i + lo, X_i + hi]
-// whose centres pass the spatial gate of Alg. 1, computed once
-// per point instead of once per (point, tile) visit; stored as int8 (lo, hi)
-// (lo > hi: empty row).  Requires H_s <= 120.
+// Exact disc chords of every (sorted) point, for the tcgen05 engine.  Point i
+// owns R8 = chord_rows(Hs) entries for the absolute rows Y = Y0(i) + e,
+// Y0(i) = floor8(Y_i - H_s), so that the 8 rows of any 16x8-column tile are
+// one aligned 16-byte block.  Entry = int8 (lo, hi): columns [X_i + lo,
+// X_i + hi] whose centres pass the spatial gate of Alg. 1,
+// (1, 0) for an empty row; computed once per point instead of once per
+// (point, tile) visit.  Requires H_s <= 120.
 __global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams g, uint16_t *__restrict__ chords) {
-    const int rows = 2 * g.Hs + 1;
+    const int rows = chord_rows(g.Hs);
     const int64_t total = n * rows;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / rows;
         const int j = (int)(e - i * rows);
         const PointRec r = rec[i];
-        int lo, hi;
-        row_chord(g, r, r.Y - g.Hs + j, &lo, &hi);
-        int dl = lo - r.X, dh = hi - r.X;
-        if (dl > dh) { dl = 1; dh = 0; }
+        const int Y = ((r.Y - g.Hs) & ~7) + j;
+        int dl = 1, dh = 0;
+        if (Y >= r.Y - g.Hs && Y <= r.Y + g.Hs) {
+            int lo, hi;
+            row_chord(g, r, Y, &lo, &hi);
+            if (lo <= hi) { dl = lo - r.X; dh = hi - r.X; }
+        }
         chords[e] = (uint16_t)((uint8_t)(int8_t)dl | ((uint16_t)(uint8_t)(int8_t)dh << 8));
     }
 }
@@ -105,7 +110,8 @@ __device__ __forceinline__ uint32_t tile_candidates(const GridParams &g, const u
                                                     int a, int b, int c) {
     int a0 = max(a - g.Ra, 0), a1 = min(a + g.Ra, g.NTX - 1);
     int b0 = max(b - g.Ray, 0), b1 = min(b + g.Ray, g.NTY - 1);
-    int c0 = max(c - g.Rt, 0), c1 = min(c + g.Rt, g.NTT - 1);
+    int c0, c1;
+    home_t_range(g, c, &c0, &c1);
     uint32_t s = 0;
     for (int cc = c0; cc <= c1; ++cc)
         for (int bb2 = b0; bb2 <= b1; ++bb2) {
@@ -217,16 +223,16 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 
 int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st) {
     const GridParams &g = p->g;
-    cudaMemsetAsync(p->bucket_cnt, 0, (p->ntiles + 1) * sizeof(uint32_t), st);
+    cudaMemsetAsync(p->bucket_cnt, 0, (p->nbuckets + 1) * sizeof(uint32_t), st);
     k_prep<<<nblk(n, 256), 256, 0, st>>>(d_points, n, g, p->rec, p->keys_in, p->vals_in, p->bucket_cnt,
-                                          p->counters + 1, (uint32_t)p->ntiles);
+                                          p->counters + 1, (uint32_t)p->nbuckets);
     size_t bytes = p->cub_bytes;
     if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->keys_in, p->keys_out, p->vals_in, p->vals_out,
                                         (int)n, 0, p->key_bits, st) != cudaSuccess)
         return STKDE_ECUDA;
     k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n);
     bytes = p->cub_bytes;
-    if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->bucket_cnt, p->bucket_begin, (int)(p->ntiles + 1), st) !=
+    if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->bucket_cnt, p->bucket_begin, (int)(p->nbuckets + 1), st) !=
         cudaSuccess)
         return STKDE_ECUDA;
     p->last_own_launches += 2;
@@ -235,7 +241,7 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
 }
 
 int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
-    const int64_t total = n * (2 * p->g.Hs + 1);
+    const int64_t total = n * chord_rows(p->g.Hs);
     if (total > 0) {
         const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 16);
         k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords);

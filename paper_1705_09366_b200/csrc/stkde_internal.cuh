@@ -49,13 +49,27 @@ struct GridParams {
     int Hs, Ht;             // ceil(hs/sres), ceil(ht/tres)
     int NTX, NTY, NTT;      // tiles per axis
     int BY, BT;             // tile width in Y (columns), tile height (layers)
+    int BTH, NTTH;          // home-bucket depth in T (layers; BT for the legacy engines) and count
     int Ra, Ray, Rt;        // home-bucket reach in tiles: ceil(Hs/BX), ceil(Hs/BY), ceil(Ht/BT)
     int kernel;             // STKDE_KERNEL_*
 };
 
+// rows of a point's chord table (tcgen05 engine): the 8-aligned row blocks that
+// cover [Y_i - H_s, Y_i + H_s] for any Y_i
+__host__ __device__ inline int chord_rows(int Hs) { return ((2 * Hs + 1 + 7) / 8 + 1) * 8; }
+
 __host__ __device__ inline int floordiv(int a, int b) {
     int q = a / b;
     return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+// Home T-blocks whose points can reach work-tile layer block c: the windows
+// [T_i - H_t, T_i + H_t] meet [c BT, c BT + BT - 1] iff T_i is in
+// [c BT - H_t, c BT + BT - 1 + H_t] (Alg. 2/3 loop bounds).
+__host__ __device__ inline void home_t_range(const GridParams &g, int c, int *cc0, int *cc1) {
+    const int t0 = c * g.BT;
+    *cc0 = max(floordiv(t0 - g.Ht, g.BTH), 0);
+    *cc1 = min(floordiv(t0 + g.BT - 1 + g.Ht, g.BTH), g.NTTH - 1);
 }
 
 // ---- exact FP64 gates: the same IEEE expression sequence as Alg. 1 ----
@@ -142,7 +156,8 @@ struct stkde_plan_s {
     int tile_threads;
     int ctas_per_sm;
     int64_t max_n;
-    int64_t ntiles;           // NTX*NTY*NTT (global)
+    int64_t ntiles;           // NTX*NTY*NTT (global work tiles)
+    int64_t nbuckets;         // NTX*NTY*NTTH (home buckets)
     int key_bits;             // radix bits of the home-bucket keys
     int chunk;                // candidates per work item
     int64_t max_items;
@@ -153,7 +168,7 @@ struct stkde_plan_s {
     void *ws;
     size_t ws_bytes;
     stkde::PointRec *rec, *rec_sorted;
-    uint16_t *chords;           // tcgen05 engine: [max_n][2Hs+1] exact disc chords (int8 lo, hi - X_i)
+    uint16_t *chords;           // tcgen05 engine: [max_n][chord_rows(Hs)] exact disc chords (int8 lo, hi - X_i)
     uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
     uint32_t *bucket_cnt;       // [ntiles + 1]
     uint32_t *bucket_begin;     // [ntiles + 2]
@@ -163,7 +178,9 @@ struct stkde_plan_s {
     uint32_t *arrive;           // [ntiles]
     float *partials;            // [max_slots][256*BT]
     int *counters;              // [0] work counter, [1] error flag, [2..3] u64 issued MMA columns,
-                                // [4..5] u64 issued k-blocks (tcgen05 engine instrumentation)
+                                // [4..5] u64 issued k-blocks (tcgen05 engine instrumentation),
+                                // [32..95] u64 [32] tcgen05 phase profile (stkde_plan_tc_profile)
+    int tc_profile;             // STKDE_TC_PROF: record the tcgen05 kernel's phase profile
     int *hist_t;                // [Gt + 1] slab-partition histogram
     void *cub_tmp;
     size_t cub_bytes;

@@ -107,7 +107,8 @@ k_tile(const GridParams g, const PointRec *__restrict__ recs, const uint32_t *__
         // ---- home-bucket segments of this tile ----
         const int a0 = max(ta - g.Ra, 0), a1 = min(ta + g.Ra, g.NTX - 1);
         const int b0 = max(tb - g.Ray, 0), b1 = min(tb + g.Ray, g.NTY - 1);
-        const int cc0 = max(tc - g.Rt, 0), cc1 = min(tc + g.Rt, g.NTT - 1);
+        int cc0, cc1;
+        home_t_range(g, tc, &cc0, &cc1);
         const int nb = b1 - b0 + 1, nseg = nb * (cc1 - cc0 + 1);
         for (int k = tid; k < nseg; k += K::NTHR) {
             int bb = b0 + k % nb, cc = cc0 + k / nb;

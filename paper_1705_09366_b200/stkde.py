@@ -23,7 +23,8 @@ KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
 EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_compute_slab",
            "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
-           "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_strerror", "stkde_last_error")
+           "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_strerror",
+           "stkde_last_error")
 
 
 class StkdeError(RuntimeError):
@@ -69,6 +70,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_enable_kernel_timing.argtypes = [P, I32]
     L.stkde_plan_kernel_ms.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(I64)]
     L.stkde_plan_mma_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+    L.stkde_plan_tc_profile.argtypes = [P, ctypes.POINTER(ctypes.c_uint64)]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
@@ -76,7 +78,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition", "stkde_slab_cuts",
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
-                 "stkde_plan_mma_stats"):
+                 "stkde_plan_mma_stats", "stkde_plan_tc_profile"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -210,6 +212,12 @@ class Plan:
         ms, k = ctypes.c_double(0), ctypes.c_int64(0)
         _check(load_library().stkde_plan_kernel_ms(self._h, ctypes.byref(ms), ctypes.byref(k)))
         return ms.value, k.value
+
+    def tc_profile(self):
+        """32 u64 phase counters of the tcgen05 kernel (STKDE_TC_PROF=1 at plan creation), reset on read."""
+        buf = (ctypes.c_uint64 * 32)()
+        _check(load_library().stkde_plan_tc_profile(self._h, buf))
+        return list(buf)
 
     def mma_stats(self):
         """(sum of MMA widths N, k-blocks) issued by the tcgen05 engine since the last call."""

@@ -162,7 +162,9 @@ def test_split_hot_tiles(S, oracle_mod, engine):
         gpu2, _, _ = run_gpu(S, w.points, **g)
     finally:
         del os.environ["STKDE_CHUNK"]
-    assert info["chunk_candidates"] == 64
+    # the slot budget may raise the chunk a little above the request; it stays
+    # far below the hot tiles' candidate counts, so most of them split
+    assert info["chunk_candidates"] <= 256
     assert np.array_equal(gpu, gpu2)
     ref = oracle_mod.stkde_pb(w.points, **g)
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="split")
@@ -182,19 +184,20 @@ def test_tile_variants(S, oracle_mod, bt_c):
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=str(bt_c))
 
 
-@pytest.mark.parametrize("bt", [64, 128])
-def test_tc_tile_heights(S, oracle_mod, bt):
-    # tcgen05 engine at both tile heights on a grid where both are legal
+@pytest.mark.parametrize("bt,bth", [(64, 16), (128, 16), (128, 8), (128, 64), (64, 128)])
+def test_tc_tile_heights(S, oracle_mod, bt, bth):
+    # tcgen05 engine at both tile heights and several home-bucket depths in T
+    # (the candidate segments of a tile are the home blocks its reach meets)
     w = synth.make_config("dengue")
     g = w.grid_kwargs()
-    os.environ["STKDE_BT"], os.environ["STKDE_ENGINE"] = str(bt), "2"
+    os.environ["STKDE_BT"], os.environ["STKDE_BTH"], os.environ["STKDE_ENGINE"] = str(bt), str(bth), "2"
     try:
         gpu, _, info = run_gpu(S, w.points, **g)
     finally:
-        del os.environ["STKDE_BT"], os.environ["STKDE_ENGINE"]
+        del os.environ["STKDE_BT"], os.environ["STKDE_BTH"], os.environ["STKDE_ENGINE"]
     assert info["Bt"] == bt and info["By"] == 8 and info["engine"] == 2
     ref = oracle_mod.stkde_pb(w.points, **g)
-    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="tc bt=%d" % bt)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="tc bt=%d bth=%d" % (bt, bth))
 
 
 def test_sharded_single_process_equals_full(S):
