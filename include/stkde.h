@@ -182,6 +182,11 @@ int stkde_plan_mma_stats(stkde_plan_t plan, int64_t *mma_columns, int64_t *kbloc
  * resets them.  Synchronises the device. */
 int stkde_plan_tc_profile(stkde_plan_t plan, uint64_t *out32);
 
+/* Development diagnostics: buf = device-accessible (e.g. pinned host) array of
+ * num_sms * 32 uint32; the tcgen05 kernel's warps publish their protocol state
+ * (tag << 24 | step) in it while running.  NULL disables. */
+int stkde_plan_debug_progress(stkde_plan_t plan, void *buf);
+
 /* Human-readable message for a return code / the last error of this thread. */
 const char *stkde_strerror(int code);
 const char *stkde_last_error(void);

@@ -220,6 +220,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     CK(cudaMemset(p->arrive, 0, nt * 4));
     CK(cudaMemset(p->counters, 0, 128 * 4));
     p->tc_profile = env_int("STKDE_TC_PROF", 0);
+    p->tc_watchdog = env_int("STKDE_TC_WATCHDOG", 0);
     *out = p;
     return STKDE_OK;
 }
@@ -487,8 +488,16 @@ extern "C" int stkde_plan_tc_profile(stkde_plan_t p, uint64_t *out32) {
     if (!p || !out32) { set_error("NULL argument"); return STKDE_EINVAL; }
     CK(cudaSetDevice(p->device));
     CK(cudaDeviceSynchronize());
-    CK(cudaMemcpy(out32, p->counters + 32, 32 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out32, p->counters + 32, 31 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(out32 + 31, p->counters + 96, sizeof(uint64_t), cudaMemcpyDeviceToHost));   // watchdog record
     CK(cudaMemset(p->counters + 32, 0, 32 * sizeof(uint64_t)));
+    CK(cudaMemset(p->counters + 96, 0, sizeof(uint64_t)));
+    return STKDE_OK;
+}
+
+extern "C" int stkde_plan_debug_progress(stkde_plan_t p, void *buf) {
+    if (!p) { set_error("NULL argument"); return STKDE_EINVAL; }
+    p->debug_progress = buf;
     return STKDE_OK;
 }
 

@@ -23,7 +23,7 @@ KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
 EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_compute_slab",
            "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
-           "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_strerror",
+           "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress", "stkde_strerror",
            "stkde_last_error")
 
 
@@ -51,6 +51,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("STKDE_LIB_PATH", path)   # development: an alternative in-tree build
     if not os.path.exists(path):
         raise FileNotFoundError("libstkde.so not built at %s (run python -m paper_1705_09366_b200.build)" % path)
     L = ctypes.CDLL(path)
@@ -71,6 +72,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_kernel_ms.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(I64)]
     L.stkde_plan_mma_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.stkde_plan_tc_profile.argtypes = [P, ctypes.POINTER(ctypes.c_uint64)]
+    L.stkde_plan_debug_progress.argtypes = [P, P]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
@@ -78,7 +80,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition", "stkde_slab_cuts",
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
-                 "stkde_plan_mma_stats", "stkde_plan_tc_profile"):
+                 "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -218,6 +220,10 @@ class Plan:
         buf = (ctypes.c_uint64 * 32)()
         _check(load_library().stkde_plan_tc_profile(self._h, buf))
         return list(buf)
+
+    def debug_progress(self, ptr: int):
+        """Development aid: device-accessible uint32[num_sms * 32] progress buffer (0 = off)."""
+        _check(load_library().stkde_plan_debug_progress(self._h, ctypes.c_void_p(ptr) if ptr else None))
 
     def mma_stats(self):
         """(sum of MMA widths N, k-blocks) issued by the tcgen05 engine since the last call."""

@@ -350,6 +350,89 @@ __global__ void k_rate_i8(int N, int nmma, long long *cyc) {
     if (warp == 0) tc::tmem_dealloc<512>(tb);
 }
 
+// latency: nm back-to-back i8 TS MMAs (N) + commit, from first issue to the
+// mbarrier completion seen by the issuing warp; repeated reps times
+__global__ void k_lat_i8(int N, int nm, int reps, long long *cyc) {
+    __shared__ __align__(1024) unsigned char sb[256 * 32];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int e = tid; e < 256 * 32 / 4; e += blockDim.x) reinterpret_cast<uint32_t *>(sb)[e] = 0x01010101u;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); }
+    tc::fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase;
+    if (warp == 0) {
+        const uint32_t id = idesc_u8(M, N);
+        const uint64_t b = tc::smem_desc(tc::smem_u32(sb), LBO, SBO);
+        long long tot = 0;
+        for (int r = 0; r < reps; ++r) {
+            long long t0 = clock64();
+            if (elect_one()) {
+                for (int i = 0; i < nm; ++i) mma_ts_i8(tb, tb + 448, b, id, 1);
+                tc::mma_commit(&bar);
+            }
+            __syncwarp();
+            tc::mbar_wait(&bar, r & 1);
+            tot += clock64() - t0;
+        }
+        if (tid == 0) cyc[0] = tot / reps;
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
+// latency of (7 MMAs + commit) while warps 4..7 stream tcgen05.st x32 into other columns
+__global__ void k_lat_st(int N, int reps, int stress_st, long long *cyc) {
+    __shared__ __align__(1024) unsigned char sb[256 * 32];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ volatile int stop;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int e = tid; e < 256 * 32 / 4; e += blockDim.x) reinterpret_cast<uint32_t *>(sb)[e] = 0x01010101u;
+    if (warp == 0) tc::tmem_alloc<512>(&tbase);
+    if (tid == 0) { tc::mbar_init(&bar, 1); tc::fence_mbar_init(); stop = 0; }
+    tc::fence_proxy_async_smem();
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tb = tbase;
+    if (warp == 0) {
+        const uint32_t id = idesc_u8(M, N);
+        const uint64_t b = tc::smem_desc(tc::smem_u32(sb), LBO, SBO);
+        long long tot = 0;
+        for (int r = 0; r < reps; ++r) {
+            long long t0 = clock64();
+            if (elect_one()) {
+                for (int i = 0; i < 7; ++i) mma_ts_i8(tb, tb + 448, b, id, 1);
+                tc::mma_commit(&bar);
+            }
+            __syncwarp();
+            tc::mbar_wait(&bar, r & 1);
+            tot += clock64() - t0;
+            for (int k = 0; k < 200; ++k) __nanosleep(10);
+        }
+        if (tid == 0) { cyc[0] = tot / reps; stop = 1; }
+    } else if (warp >= 4 && stress_st) {
+        uint32_t v[32];
+        for (int j = 0; j < 32; ++j) v[j] = j;
+        const uint32_t addr = tb + ((uint32_t)(32 * (warp & 3)) << 16) + 384;
+        while (!stop) {
+            tc::tmem_st32(addr, v);
+            tc::tmem_wait_st();
+        }
+    }
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    if (warp == 0) tc::tmem_dealloc<512>(tb);
+}
+
 static float frand(unsigned &s) { s = s * 1664525u + 1013904223u; return (float)((int)((s >> 16) % 5) - 2); }
 
 int main() {
@@ -481,6 +564,19 @@ int main() {
             cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
             printf("i8 TS N=%3d: %.2f cycles per MMA (K=32)\n", N, (double)hc / nm);
         }
+    }
+    for (int N : {16, 64, 128})
+        for (int nm : {1, 7, 14}) {
+            k_lat_i8<<<1, 128>>>(N, nm, 64, dc);
+            if (cudaDeviceSynchronize() != cudaSuccess) { printf("lat: error\n"); return 1; }
+            cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+            printf("i8 latency N=%3d, %2d MMAs + commit: %lld cycles (floor %d)\n", N, nm, hc, nm * N / 2);
+        }
+    for (int st = 0; st < 2; ++st) {
+        k_lat_st<<<1, 256>>>(64, 64, st, dc);
+        if (cudaDeviceSynchronize() != cudaSuccess) { printf("latst: error\n"); return 1; }
+        cudaMemcpy(&hc, dc, 8, cudaMemcpyDeviceToHost);
+        printf("i8 latency N=64, 7 MMAs + commit, %s: %lld cycles\n", st ? "with tcgen05.st traffic" : "idle", hc);
     }
     printf(fails ? "PROBE FAIL\n" : "PROBE OK\n");
     return fails != 0;
