@@ -97,9 +97,30 @@ __global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams
         const int Y = ((r.Y - g.Hs) & ~7) + j;
         int dl = 1, dh = 0;
         if (Y >= r.Y - g.Hs && Y <= r.Y + g.Hs) {
-            int lo, hi;
-            row_chord(g, r, Y, &lo, &hi);
-            if (lo <= hi) { dl = lo - r.X; dh = hi - r.X; }
+            // FP32 fast path in voxel-local coordinates: column X_i + k is inside iff
+            // (k - pc)^2 + dy^2 < r^2 with pc = fx - 0.5; it is exact unless a decision
+            // falls within the FP64 band (then row_chord re-decides with Alg. 1's FP64 gate)
+            const float dyv = (float)(Y - r.Y) + 0.5f - r.fy;
+            const float dy2 = __fmul_rn(dyv, dyv);
+            const float lo_b = g.rs2 * (1.0f - GATE_BAND), hi_b = g.rs2 * (1.0f + GATE_BAND);
+            bool exact = false;
+            if (dy2 > hi_b) {
+                exact = true;                                  // empty row
+            } else if (dy2 < lo_b) {
+                const float pc = r.fx - 0.5f;
+                const float c = sqrtf(g.rs2 - dy2);
+                const int a = (int)floorf(pc - c) + 1, b = (int)ceilf(pc + c) - 1;
+                auto d2 = [&](int k) { const float dx = (float)k - pc; return __fadd_rn(__fmul_rn(dx, dx), dy2); };
+                if (a <= b && d2(a) < lo_b && d2(b) < lo_b && d2(a - 1) > hi_b && d2(b + 1) > hi_b) {
+                    dl = a; dh = b;
+                    exact = true;
+                }
+            }
+            if (!exact) {
+                int lo, hi;
+                row_chord(g, r, Y, &lo, &hi);
+                if (lo <= hi) { dl = lo - r.X; dh = hi - r.X; }
+            }
         }
         chords[e] = (uint16_t)((uint8_t)(int8_t)dl | ((uint16_t)(uint8_t)(int8_t)dh << 8));
     }
