@@ -65,8 +65,9 @@ enum {
  * TENSOR: the per-tile contraction on the legacy tensor-core path (mma.sync
  * m16n8k16, FP16 3-term split, FP32 accumulation; 16x16 columns) -- DESIGN.md
  * §3.5.  TC: the same contraction on 5th-generation tensor cores (tcgen05.mma
- * kind::f16, M = 128 columns of a 16x8-column tile, A generated into TMEM,
- * accumulator in TMEM) -- DESIGN.md §3.6.  All engines compute the same sums
+ * kind::i8, 23-bit fixed-point factors split into three 8-bit limbs, exact S32
+ * accumulation in TMEM; M = 128 columns of a 16x8-column tile, A generated
+ * into TMEM) -- DESIGN.md §3.6.  Hs > 120 falls back to TENSOR.  All engines compute the same sums
  * within the parity tolerance; they differ in speed only. */
 enum { STKDE_ENGINE_SIMT = 0, STKDE_ENGINE_TENSOR = 1, STKDE_ENGINE_TC = 2 };
 
