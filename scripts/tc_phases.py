@@ -27,15 +27,13 @@ for name in sys.argv[1:] or ["stress"]:
         v = p.tc_profile()
         gt, lt = v[10] or 1, v[23] or 1
         print("%s: generators (sum over teams, cycles): %s" % (name, ", ".join(
-            "%s %.1f%%" % (n, 100.0 * v[i] / gt) for i, n in enumerate(GEN[:8]))))
-        print("    k-blocks %d, per k-block per team %.0f cycles; post->MMA issued %.0f, issued->stage free seen %.0f" % (
-            v[8], v[10] / max(v[8], 1) * 1.0, v[14] / max(v[8], 1), v[11] / max(v[8], 1)))
+            "%s %.1f%%" % (n, 100.0 * (v[i] + (v[11] + v[12] + v[13] + v[14] if i == 7 else 0)) / gt)
+            for i, n in enumerate(GEN[:8]))))
+        print("    k-blocks %d, per k-block per team %.0f cycles" % (v[8], v[10] / max(v[8], 1) * 1.0))
         print("%s: loader: %s, batches %d" % (name, ", ".join(
             "%s %.1f%%" % (n, 100.0 * v[16 + i] / lt) for i, n in list(enumerate(LD))[:6] + [(8, "wait_tma")]),
             v[22]))
-        mt = v[29] or 1
-        print("%s: MMA warp: wait_full %.1f%%, poll %.1f%%, issue %.1f%%, dfree_wait %.1f%%, other %.1f%%" % (
-            name, 100.0 * v[24] / mt, 100.0 * v[25] / mt, 100.0 * v[26] / mt, 100.0 * v[27] / mt, 100.0 * v[28] / mt))
-        print("    per k-block: setup %.0f cycles, mma+commit %.0f cycles" % (v[12] / max(v[8], 1), v[13] / max(v[8], 1)))
+        print("    epilogue: wait+sync %.1f%%, tmem ld+cvt %.1f%%, bulk read wait %.1f%%, stage+issue %.1f%%, tail %.1f%%"
+              % tuple(100.0 * v[i] / gt for i in (11, 12, 14, 13, 7)))
         print("    stage waits > 200 cycles: %d of %d k-blocks (%d at a batch's first k-block)" % (
             v[9] >> 40, v[8], (v[9] >> 20) & 0xFFFFF))
