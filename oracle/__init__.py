@@ -55,7 +55,13 @@ def _L():
         _lib.oracle_k_t.restype = D
         _lib.oracle_H.argtypes = [D, D]
         _lib.oracle_H.restype = I64
-        for f in (_lib.oracle_pb, _lib.oracle_vb, _lib.oracle_vb_voxels, _lib.oracle_contributions):
+        _lib.oracle_pb_adaptive.argtypes = [P, P, I64, P, P, P, P, P, I32]
+        _lib.oracle_vb_adaptive.argtypes = [P, P, I64, P, P, P, P, P]
+        _lib.oracle_vb_voxels_adaptive.argtypes = [P, P, I64, P, P, I64, P, P, P, I32]
+        _lib.oracle_contributions_adaptive.argtypes = [P, P, I64, P, P, I32]
+        for f in (_lib.oracle_pb, _lib.oracle_vb, _lib.oracle_vb_voxels, _lib.oracle_contributions,
+                  _lib.oracle_pb_adaptive, _lib.oracle_vb_adaptive, _lib.oracle_vb_voxels_adaptive,
+                  _lib.oracle_contributions_adaptive):
             f.restype = I32
     return _lib
 
@@ -72,6 +78,20 @@ def _pts(points):
 
 def _ptr(a):
     return None if a is None else a.ctypes.data
+
+
+def _bw(bw, n):
+    b = np.ascontiguousarray(bw, dtype=np.float32).reshape(-1, 2)
+    if b.shape[0] != n:
+        raise ValueError("bw must be float32 [n][2] = (hs_i, ht_i)")
+    return b, b.ctypes.data
+
+
+def _rc(rc, what):
+    if rc == -3:
+        raise ValueError("%s: per-point bandwidths must satisfy 0 < hs_i <= hs, 0 < ht_i <= ht" % what)
+    if rc != 0:
+        raise ValueError("%s failed: %d" % (what, rc))
 
 
 class OracleResult:
@@ -147,3 +167,64 @@ def k_t(w, kernel=0) -> float:
 
 def H(h, res) -> int:
     return _L().oracle_H(float(h), float(res))
+
+
+# ---- adaptive bandwidth (reading R15) ----
+# bw = float32 [n][2] = (hs_i, ht_i) in world units, each <= the grid's (hs, ht),
+# which then only bound the loops.  f = 1/n sum_i k_s k_t / (hs_i^2 ht_i).
+
+def stkde_pb_adaptive(points, bw, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel=0,
+                      with_ambiguity=True, nthreads=0) -> OracleResult:
+    """Point-major FP64 adaptive-bandwidth density (bitwise equal to stkde_vb_adaptive)."""
+    p, pp = _pts(points)
+    b, bp = _bw(bw, p.shape[0])
+    g = _grid(x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel)
+    vol = np.empty((Gx, Gy, Gt), dtype=np.float64)
+    slack = np.empty_like(vol) if with_ambiguity else None
+    amb = np.empty((Gx, Gy, Gt), dtype=np.uint8) if with_ambiguity else None
+    C = ctypes.c_int64(0)
+    _rc(_L().oracle_pb_adaptive(pp, bp, p.shape[0], ctypes.byref(g), vol.ctypes.data, _ptr(slack), _ptr(amb),
+                                ctypes.addressof(C), int(nthreads)), "oracle_pb_adaptive")
+    return OracleResult(vol, slack, amb, C.value)
+
+
+def stkde_vb_adaptive(points, bw, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel=0) -> OracleResult:
+    """Alg. 1 brute force with per-point bandwidths (tiny grids only)."""
+    p, pp = _pts(points)
+    b, bp = _bw(bw, p.shape[0])
+    g = _grid(x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel)
+    vol = np.empty((Gx, Gy, Gt), dtype=np.float64)
+    slack = np.empty_like(vol)
+    amb = np.empty((Gx, Gy, Gt), dtype=np.uint8)
+    C = ctypes.c_int64(0)
+    _rc(_L().oracle_vb_adaptive(pp, bp, p.shape[0], ctypes.byref(g), vol.ctypes.data, slack.ctypes.data,
+                                amb.ctypes.data, ctypes.addressof(C)), "oracle_vb_adaptive")
+    return OracleResult(vol, slack, amb, C.value)
+
+
+def stkde_vb_voxels_adaptive(points, bw, voxels, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel=0,
+                             nthreads=0):
+    """Adaptive Alg. 1 at the given linear voxel indices -> (values, slack, amb)."""
+    p, pp = _pts(points)
+    b, bp = _bw(bw, p.shape[0])
+    g = _grid(x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel)
+    vox = np.ascontiguousarray(voxels, dtype=np.int64)
+    val = np.empty(len(vox), dtype=np.float64)
+    slack = np.empty(len(vox), dtype=np.float64)
+    amb = np.empty(len(vox), dtype=np.uint8)
+    _rc(_L().oracle_vb_voxels_adaptive(pp, bp, p.shape[0], ctypes.byref(g), vox.ctypes.data, len(vox),
+                                       val.ctypes.data, slack.ctypes.data, amb.ctypes.data, int(nthreads)),
+        "oracle_vb_voxels_adaptive")
+    return val, slack, amb
+
+
+def contributions_adaptive(points, bw, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel=0,
+                           nthreads=0) -> int:
+    """Exact number of gated (point, voxel) pairs with per-point bandwidths."""
+    p, pp = _pts(points)
+    b, bp = _bw(bw, p.shape[0])
+    g = _grid(x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht, kernel)
+    C = ctypes.c_int64(0)
+    _rc(_L().oracle_contributions_adaptive(pp, bp, p.shape[0], ctypes.byref(g), ctypes.addressof(C),
+                                           int(nthreads)), "oracle_contributions_adaptive")
+    return C.value

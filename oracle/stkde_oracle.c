@@ -36,6 +36,20 @@
  *               oracle_vb and independent of the thread count.
  * oracle_vb_voxels : Alg. 1 at a caller-chosen list of voxels (full-size sampling).
  *
+ * Adaptive bandwidth (PAPER.md:1060-1062 names "a bandwidth
+ * that adapts to the density of population" as future work; reading R15 in
+ * DESIGN.md): point i carries its own (hs_i, ht_i) and the density is the
+ * sample-point estimator
+ *
+ *   f(X,Y,T) = 1/n * sum_{i : d < hs_i and |dt| <= ht_i}
+ *                  k_s(|dx|/hs_i, |dy|/hs_i) k_t(|dt|/ht_i) / (hs_i^2 ht_i),
+ *
+ * which is PAPER.md:120-121 with h_s, h_t moved inside the sum (equal to it
+ * when every hs_i = hs, ht_i = ht).  oracle_*_adaptive take bw = float[n][2]
+ * (hs_i, ht_i), widened exactly to FP64; the grid's hs/ht only bound the loops
+ * (every hs_i <= hs, ht_i <= ht; violations return -3).  Each term is
+ * (k_s k_t) / (hs_i*hs_i*ht_i), summed in input order, then divided by n.
+ *
  * Optional outputs: per-voxel ambiguity flag and slack (reading R10/R11):
  * a (point, voxel) pair is ambiguous when |sqrt(d^2)/hs - 1| <= 1e-6 or
  * ||dt|/ht - 1| <= 1e-6 while the other coordinate is inside (or itself
@@ -93,24 +107,39 @@ int oracle_check_grid(const oracle_grid_t *g) {
 
 /* Per-pair evaluation shared by VB and PB (same expressions, same order).
  * Spatial half of a (point, voxel) pair: gate, ambiguity, and k_s. */
-static int eval_pair(const oracle_grid_t *g, double px, double py, int64_t X, int64_t Y,
+static int eval_pair(const oracle_grid_t *g, double hs, double px, double py, int64_t X, int64_t Y,
                      double *ksv, int *s_amb_out, int *s_in_out) {
     double dx = cx(g, X) - px;
     double dy = cy(g, Y) - py;
     double d = sqrt(dx * dx + dy * dy);       /* Alg. 1 gate */
-    int s_in = d < g->hs;
-    int s_amb = fabs(d / g->hs - 1.0) <= ORACLE_AMB_REL;
+    int s_in = d < hs;
+    int s_amb = fabs(d / hs - 1.0) <= ORACLE_AMB_REL;
     *s_in_out = s_in;
     *s_amb_out = s_amb;
-    if (s_in || s_amb) *ksv = k_s(g, fabs(dx) / g->hs, fabs(dy) / g->hs);
+    if (s_in || s_amb) *ksv = k_s(g, fabs(dx) / hs, fabs(dy) / hs);
     else *ksv = 0.0;
     return s_in;
 }
 
+/* Per-point bandwidths of the adaptive estimator (NULL bw: the grid's). */
+static void point_bw(const oracle_grid_t *g, const float *bw, int64_t i, double *hs, double *ht) {
+    if (bw) { *hs = (double)bw[2 * i]; *ht = (double)bw[2 * i + 1]; }
+    else { *hs = g->hs; *ht = g->ht; }
+}
+static int check_bw(const oracle_grid_t *g, const float *bw, int64_t n) {
+    if (!bw) return 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double hs = bw[2 * i], ht = bw[2 * i + 1];
+        if (!(hs > 0) || !(ht > 0) || hs > g->hs || ht > g->ht) return -3;
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------------ VB --- */
-int oracle_vb(const float *pts, int64_t n, const oracle_grid_t *g,
-              double *vol, double *slack, uint8_t *amb, int64_t *contributions) {
+static int vb_impl(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                   double *vol, double *slack, uint8_t *amb, int64_t *contributions) {
     if (oracle_check_grid(g)) return -1;
+    if (check_bw(g, bw, n)) return -3;
     const int64_t Gx = g->Gx, Gy = g->Gy, Gt = g->Gt;
     const double den = (double)n * (g->hs * g->hs) * g->ht;
     int64_t C = 0;
@@ -121,28 +150,44 @@ int oracle_vb(const float *pts, int64_t n, const oracle_grid_t *g,
                 int a = 0;
                 for (int64_t i = 0; i < n; ++i) {
                     double px = pts[3 * i], py = pts[3 * i + 1], pt = pts[3 * i + 2];
+                    double hs, ht;
+                    point_bw(g, bw, i, &hs, &ht);
                     double dt = fabs(ct(g, T) - pt);
-                    int t_in = dt <= g->ht;
-                    int t_amb = fabs(dt / g->ht - 1.0) <= ORACLE_AMB_REL;
+                    int t_in = dt <= ht;
+                    int t_amb = fabs(dt / ht - 1.0) <= ORACLE_AMB_REL;
                     if (!t_in && !t_amb) continue;
                     double ksv; int s_amb, s_in;
-                    eval_pair(g, px, py, X, Y, &ksv, &s_amb, &s_in);
+                    eval_pair(g, hs, px, py, X, Y, &ksv, &s_amb, &s_in);
+                    /* fixed bandwidth: sum k_s k_t, divide by n hs^2 ht at the end;
+                       adaptive: each term divided by its own hs_i^2 ht_i, then by n */
+                    const double dn = bw ? hs * hs * ht : 1.0;
                     if (s_in && t_in) {
-                        sum += ksv * k_t(g, dt / g->ht);
+                        sum += bw ? ksv * k_t(g, dt / ht) / dn : ksv * k_t(g, dt / ht);
                         ++C;
                     }
                     if ((s_amb && (t_in || t_amb)) || (t_amb && (s_in || s_amb))) {
                         a = 1;
-                        sl += fabs(ksv * k_t(g, dt / g->ht));
+                        sl += bw ? fabs(ksv * k_t(g, dt / ht)) / dn : fabs(ksv * k_t(g, dt / ht));
                     }
                 }
                 int64_t v = (X * Gy + Y) * Gt + T;
-                vol[v] = n > 0 ? sum / den : 0.0;
-                if (slack) slack[v] = n > 0 ? sl / den : 0.0;
+                const double dd = bw ? (double)n : den;
+                vol[v] = n > 0 ? sum / dd : 0.0;
+                if (slack) slack[v] = n > 0 ? sl / dd : 0.0;
                 if (amb) amb[v] = (uint8_t)a;
             }
     if (contributions) *contributions = C;
     return 0;
+}
+
+int oracle_vb(const float *pts, int64_t n, const oracle_grid_t *g,
+              double *vol, double *slack, uint8_t *amb, int64_t *contributions) {
+    return vb_impl(pts, NULL, n, g, vol, slack, amb, contributions);
+}
+int oracle_vb_adaptive(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                       double *vol, double *slack, uint8_t *amb, int64_t *contributions) {
+    if (!bw) return -1;
+    return vb_impl(pts, bw, n, g, vol, slack, amb, contributions);
 }
 
 /* ------------------------------------------------------------------ PB --- */
@@ -162,10 +207,11 @@ static int64_t clamp64(double v, int64_t lo, int64_t hi) {
     return (int64_t)v;
 }
 
-int oracle_pb(const float *pts, int64_t n, const oracle_grid_t *g,
-              double *vol, double *slack, uint8_t *amb, int64_t *contributions,
-              int nthreads) {
+static int pb_impl(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                   double *vol, double *slack, uint8_t *amb, int64_t *contributions,
+                   int nthreads) {
     if (oracle_check_grid(g)) return -1;
+    if (check_bw(g, bw, n)) return -3;
     const int64_t Gx = g->Gx, Gy = g->Gy, Gt = g->Gt;
     const int64_t Hs = oracle_H(g->hs, g->sres), Ht = oracle_H(g->ht, g->tres);
     const int64_t nvox = Gx * Gy * Gt;
@@ -220,38 +266,46 @@ int oracle_pb(const float *pts, int64_t n, const oracle_grid_t *g,
             for (int64_t k = 0; k < nc; ++k) {
                 const int64_t i = cand[k];
                 const double px = pts[3 * i], py = pts[3 * i + 1], pt = pts[3 * i + 2];
+                double hs, ht;
+                point_bw(g, bw, i, &hs, &ht);
+                /* the point's own box (adaptive: H_s(i) = ceil(hs_i/sres) <= H_s) */
+                const int64_t Hsi = bw ? oracle_H(hs, g->sres) : Hs, Hti = bw ? oracle_H(ht, g->tres) : Ht;
+                const double dn = bw ? hs * hs * ht : 1.0;
                 const int64_t Xi = clamp64(floor((px - g->x0) / g->sres), -BIG, BIG);
                 const int64_t Yi = clamp64(floor((py - g->y0) / g->sres), -(Gy + Hs + 2), Gy + Hs + 2);
                 const int64_t Ti = clamp64(floor((pt - g->t0) / g->tres), -(Gt + Ht + 2), Gt + Ht + 2);
-                const int64_t X0 = Xi - Hs > xa ? Xi - Hs : xa, X1 = Xi + Hs < xb - 1 ? Xi + Hs : xb - 1;
-                const int64_t Y0 = Yi - Hs > 0 ? Yi - Hs : 0, Y1 = Yi + Hs < Gy - 1 ? Yi + Hs : Gy - 1;
-                const int64_t T0 = Ti - Ht > 0 ? Ti - Ht : 0, T1 = Ti + Ht < Gt - 1 ? Ti + Ht : Gt - 1;
+                const int64_t X0 = Xi - Hsi > xa ? Xi - Hsi : xa, X1 = Xi + Hsi < xb - 1 ? Xi + Hsi : xb - 1;
+                const int64_t Y0 = Yi - Hsi > 0 ? Yi - Hsi : 0, Y1 = Yi + Hsi < Gy - 1 ? Yi + Hsi : Gy - 1;
+                const int64_t T0 = Ti - Hti > 0 ? Ti - Hti : 0, T1 = Ti + Hti < Gt - 1 ? Ti + Hti : Gt - 1;
                 if (X0 > X1 || Y0 > Y1 || T0 > T1) continue;
                 /* K_t[T] once per point (Alg. 3) */
                 int any_t = 0;
                 for (int64_t T = T0; T <= T1; ++T) {
                     double dt = fabs(ct(g, T) - pt);
-                    tin[T - T0] = dt <= g->ht;
-                    tam[T - T0] = fabs(dt / g->ht - 1.0) <= ORACLE_AMB_REL;
-                    kt[T - T0] = k_t(g, dt / g->ht);
+                    tin[T - T0] = dt <= ht;
+                    tam[T - T0] = fabs(dt / ht - 1.0) <= ORACLE_AMB_REL;
+                    kt[T - T0] = k_t(g, dt / ht);
                     any_t |= tin[T - T0] | tam[T - T0];
                 }
                 if (!any_t) continue;
                 for (int64_t X = X0; X <= X1; ++X)
                     for (int64_t Y = Y0; Y <= Y1; ++Y) {
                         double ksv; int s_amb, s_in;
-                        eval_pair(g, px, py, X, Y, &ksv, &s_amb, &s_in);
+                        eval_pair(g, hs, px, py, X, Y, &ksv, &s_amb, &s_in);
                         if (!s_in && !s_amb) continue;
                         double *col = vol + (X * Gy + Y) * Gt;
                         if (s_in)
                             for (int64_t T = T0; T <= T1; ++T)
-                                if (tin[T - T0]) { col[T] += ksv * kt[T - T0]; ++Ctot; }
+                                if (tin[T - T0]) {
+                                    col[T] += bw ? ksv * kt[T - T0] / dn : ksv * kt[T - T0];
+                                    ++Ctot;
+                                }
                         if (slack || amb)
                             for (int64_t T = T0; T <= T1; ++T) {
                                 int ti = tin[T - T0], ta = tam[T - T0];
                                 if ((s_amb && (ti || ta)) || (ta && (s_in || s_amb))) {
                                     int64_t v = (X * Gy + Y) * Gt + T;
-                                    if (slack) slack[v] += fabs(ksv * kt[T - T0]);
+                                    if (slack) slack[v] += bw ? fabs(ksv * kt[T - T0]) / dn : fabs(ksv * kt[T - T0]);
                                     if (amb) amb[v] = 1;
                                 }
                             }
@@ -262,20 +316,34 @@ int oracle_pb(const float *pts, int64_t n, const oracle_grid_t *g,
     }
     free(order);
     if (err) return -2;
+    const double dd = bw ? (double)n : den;
 #pragma omp parallel for schedule(static)
     for (int64_t v = 0; v < nvox; ++v) {
-        vol[v] = vol[v] / den;
-        if (slack) slack[v] = slack[v] / den;
+        vol[v] = vol[v] / dd;
+        if (slack) slack[v] = slack[v] / dd;
     }
     if (contributions) *contributions = Ctot;
     return 0;
 }
 
+int oracle_pb(const float *pts, int64_t n, const oracle_grid_t *g,
+              double *vol, double *slack, uint8_t *amb, int64_t *contributions,
+              int nthreads) {
+    return pb_impl(pts, NULL, n, g, vol, slack, amb, contributions, nthreads);
+}
+int oracle_pb_adaptive(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                       double *vol, double *slack, uint8_t *amb, int64_t *contributions,
+                       int nthreads) {
+    if (!bw) return -1;
+    return pb_impl(pts, bw, n, g, vol, slack, amb, contributions, nthreads);
+}
+
 /* ---------------------------------------------------- VB at sampled voxels --- */
-int oracle_vb_voxels(const float *pts, int64_t n, const oracle_grid_t *g,
-                     const int64_t *vox, int64_t m, double *val, double *slack,
-                     uint8_t *amb, int nthreads) {
+static int vb_voxels_impl(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                          const int64_t *vox, int64_t m, double *val, double *slack,
+                          uint8_t *amb, int nthreads) {
     if (oracle_check_grid(g)) return -1;
+    if (check_bw(g, bw, n)) return -3;
     const int64_t Gy = g->Gy, Gt = g->Gt;
     const double den = (double)n * (g->hs * g->hs) * g->ht;
 #ifdef _OPENMP
@@ -289,29 +357,45 @@ int oracle_vb_voxels(const float *pts, int64_t n, const oracle_grid_t *g,
         int a = 0;
         for (int64_t i = 0; i < n; ++i) {
             double px = pts[3 * i], py = pts[3 * i + 1], pt = pts[3 * i + 2];
+            double hs, ht;
+            point_bw(g, bw, i, &hs, &ht);
             double dt = fabs(ct(g, T) - pt);
-            int t_in = dt <= g->ht;
-            int t_amb = fabs(dt / g->ht - 1.0) <= ORACLE_AMB_REL;
+            int t_in = dt <= ht;
+            int t_amb = fabs(dt / ht - 1.0) <= ORACLE_AMB_REL;
             if (!t_in && !t_amb) continue;
             double ksv; int s_amb, s_in;
-            eval_pair(g, px, py, X, Y, &ksv, &s_amb, &s_in);
-            if (s_in && t_in) sum += ksv * k_t(g, dt / g->ht);
+            eval_pair(g, hs, px, py, X, Y, &ksv, &s_amb, &s_in);
+            const double dn = bw ? hs * hs * ht : 1.0;
+            if (s_in && t_in) sum += bw ? ksv * k_t(g, dt / ht) / dn : ksv * k_t(g, dt / ht);
             if ((s_amb && (t_in || t_amb)) || (t_amb && (s_in || s_amb))) {
                 a = 1;
-                sl += fabs(ksv * k_t(g, dt / g->ht));
+                sl += bw ? fabs(ksv * k_t(g, dt / ht)) / dn : fabs(ksv * k_t(g, dt / ht));
             }
         }
-        val[k] = n > 0 ? sum / den : 0.0;
-        if (slack) slack[k] = n > 0 ? sl / den : 0.0;
+        const double dd = bw ? (double)n : den;
+        val[k] = n > 0 ? sum / dd : 0.0;
+        if (slack) slack[k] = n > 0 ? sl / dd : 0.0;
         if (amb) amb[k] = (uint8_t)a;
     }
     return 0;
 }
+int oracle_vb_voxels(const float *pts, int64_t n, const oracle_grid_t *g,
+                     const int64_t *vox, int64_t m, double *val, double *slack,
+                     uint8_t *amb, int nthreads) {
+    return vb_voxels_impl(pts, NULL, n, g, vox, m, val, slack, amb, nthreads);
+}
+int oracle_vb_voxels_adaptive(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                              const int64_t *vox, int64_t m, double *val, double *slack,
+                              uint8_t *amb, int nthreads) {
+    if (!bw) return -1;
+    return vb_voxels_impl(pts, bw, n, g, vox, m, val, slack, amb, nthreads);
+}
 
 /* Exact gated-pair count C = sum_i (#disc columns in grid) * (#window layers in grid). */
-int oracle_contributions(const float *pts, int64_t n, const oracle_grid_t *g,
-                         int64_t *out, int nthreads) {
+static int contributions_impl(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                              int64_t *out, int nthreads) {
     if (oracle_check_grid(g)) return -1;
+    if (check_bw(g, bw, n)) return -3;
     const int64_t Hs = oracle_H(g->hs, g->sres), Ht = oracle_H(g->ht, g->tres);
     int64_t C = 0;
 #ifdef _OPENMP
@@ -320,6 +404,8 @@ int oracle_contributions(const float *pts, int64_t n, const oracle_grid_t *g,
 #pragma omp parallel for schedule(dynamic, 256) reduction(+ : C)
     for (int64_t i = 0; i < n; ++i) {
         const double px = pts[3 * i], py = pts[3 * i + 1], pt = pts[3 * i + 2];
+        double hs, ht;
+        point_bw(g, bw, i, &hs, &ht);
         const int64_t Xi = clamp64(floor((px - g->x0) / g->sres), -(g->Gx + Hs + 2), g->Gx + Hs + 2);
         const int64_t Yi = clamp64(floor((py - g->y0) / g->sres), -(g->Gy + Hs + 2), g->Gy + Hs + 2);
         const int64_t Ti = clamp64(floor((pt - g->t0) / g->tres), -(g->Gt + Ht + 2), g->Gt + Ht + 2);
@@ -329,17 +415,26 @@ int oracle_contributions(const float *pts, int64_t n, const oracle_grid_t *g,
             for (int64_t Y = Yi - Hs; Y <= Yi + Hs; ++Y) {
                 if (Y < 0 || Y >= g->Gy) continue;
                 double dx = cx(g, X) - px, dy = cy(g, Y) - py;
-                if (sqrt(dx * dx + dy * dy) < g->hs) ++cols;
+                if (sqrt(dx * dx + dy * dy) < hs) ++cols;
             }
         }
         for (int64_t T = Ti - Ht; T <= Ti + Ht; ++T) {
             if (T < 0 || T >= g->Gt) continue;
-            if (fabs(ct(g, T) - pt) <= g->ht) ++lay;
+            if (fabs(ct(g, T) - pt) <= ht) ++lay;
         }
         C += cols * lay;
     }
     *out = C;
     return 0;
+}
+int oracle_contributions(const float *pts, int64_t n, const oracle_grid_t *g,
+                         int64_t *out, int nthreads) {
+    return contributions_impl(pts, NULL, n, g, out, nthreads);
+}
+int oracle_contributions_adaptive(const float *pts, const float *bw, int64_t n, const oracle_grid_t *g,
+                                  int64_t *out, int nthreads) {
+    if (!bw) return -1;
+    return contributions_impl(pts, bw, n, g, out, nthreads);
 }
 
 /* Single kernel evaluations, exported for the closed-form pins. */
