@@ -51,7 +51,9 @@ enum {
     STKDE_ENOMEM = -2,      /* device allocation failed                              */
     STKDE_ECUDA = -3,       /* a CUDA runtime call failed                            */
     STKDE_ECAPACITY = -4,   /* n exceeds the plan's max_n                            */
-    STKDE_ENONFINITE = -5   /* some input coordinate was NaN/Inf (stkde_plan_check)  */
+    STKDE_ENONFINITE = -5,  /* some input coordinate was NaN/Inf (stkde_plan_check)  */
+    STKDE_EBANDWIDTH = -6   /* an adaptive call had a per-point bandwidth outside the
+                               plan's range (stkde_plan_check)                      */
 };
 
 /* Kernel pair (reading R1 in DESIGN.md). */
@@ -129,6 +131,43 @@ int stkde_slab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, int Bt, int Ht, double r
 int stkde_count_contributions(stkde_plan_t plan, const float *d_points, int64_t n,
                               int64_t t_begin, int64_t t_end, int64_t *d_count,
                               void *stream);
+
+/* ---- Adaptive bandwidth (reading R15) ----
+ * PAPER.md:1060-1062 names "a bandwidth that adapts to the density of
+ * population" as future work.  Point i carries its own (hs_i, ht_i) and
+ *
+ *   f(X,Y,T) = 1/n * sum_{i : d < hs_i and |dt| <= ht_i}
+ *                  k_s(|dx|/hs_i, |dy|/hs_i) * k_t(|dt|/ht_i) / (hs_i^2 ht_i),
+ *
+ * i.e. PAPER.md:120-121 with the bandwidths inside the sum (identical to it when
+ * every hs_i = hs, ht_i = ht).  d_bw is float32 [n][2] = (hs_i, ht_i) in world
+ * units on the plan's device, read-only; every pair must satisfy
+ * 0 < hs_i <= hs and 0 < ht_i <= ht of the plan (the plan's bandwidths size the
+ * binning reach).  A point violating this is skipped and raises the plan's
+ * error flag: stkde_plan_check returns STKDE_EBANDWIDTH.  Same grid layout,
+ * overwrite, asynchrony, determinism and slab rules as stkde_compute /
+ * stkde_compute_slab.  Needs the tcgen05 engine (H_s <= 120); otherwise
+ * STKDE_EINVAL. */
+int stkde_compute_adaptive(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
+                           float *d_grid, void *stream);
+int stkde_compute_adaptive_slab(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
+                                int64_t n_norm, int64_t t_begin, int64_t t_end, float *d_slab, void *stream);
+/* Exact gated-pair count C of the adaptive estimator (per-point gates). */
+int stkde_count_contributions_adaptive(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
+                                       int64_t t_begin, int64_t t_end, int64_t *d_count, void *stream);
+
+/* ---- Multi-bandwidth sweep (Fig. 1, PAPER.md:135-146:
+ * the same events viewed at several bandwidths; the Lb/Hb/VHb instances of
+ * PAPER.md:651-653) ----
+ * Bins the points ONCE at the plan's bandwidths and computes nbw full grids,
+ * grid k for bandwidths (h_hs[k], h_ht[k]) (host arrays, world units,
+ * 0 < h_hs[k] <= hs, 0 < h_ht[k] <= ht), each normalised by 1/(n h_hs[k]^2
+ * h_ht[k]).  d_grids is a host array of nbw device pointers, each float32
+ * [Gx][Gy][Gt], fully overwritten.  Asynchronous on `stream`; grid k equals
+ * stkde_compute on a plan created with (h_hs[k], h_ht[k]) within the parity
+ * tolerance.  Errors: STKDE_EINVAL (bad bandwidth / NULL grid), STKDE_ECAPACITY. */
+int stkde_compute_sweep(stkde_plan_t plan, const float *d_points, int64_t n, int nbw, const double *h_hs,
+                        const double *h_ht, float *const *d_grids, void *stream);
 
 /* Single-process multi-device driver: plans[d] lives on device d's ordinal,
  * d_points[d] holds the full point set on that device, d_slabs[d] receives

@@ -147,8 +147,9 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     const size_t tile_bytes = (size_t)(p->engine == STKDE_ENGINE_TC ? 128 : 256) * BT * 4;
     const int64_t slot_budget = (int64_t)env_int("STKDE_SLOT_MB", 1024) * (1 << 20) / (int64_t)tile_bytes;
     int64_t chunk = std::max<int64_t>(env_int("STKDE_CHUNK", 4096), (2 * cand_bound + slot_budget - 1) / slot_budget);
-    // tcgen05 engine: the S32 accumulators take <= 129796 per point,
-    // so a work item may accumulate at most 16545 points before 2^31.
+    // tcgen05 engine: the S32 accumulators take <= 129888 per point (D16: hl + mm + lh
+    // + the ICOMP = 93 indicator), so a work item may accumulate at most
+    // 16533 points before 2^31.
     if (p->engine == STKDE_ENGINE_TC) chunk = std::min<int64_t>(chunk, 16384);
     chunk = std::min<int64_t>(chunk, (int64_t)1 << 30);
     p->chunk = (int)chunk;
@@ -189,6 +190,8 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
         {(void **)&p->rec, nrec * sizeof(PointRec)},
         {(void **)&p->rec_sorted, nrec * sizeof(PointRec)},
         {(void **)&p->chords, p->engine == STKDE_ENGINE_TC ? nrec * (size_t)chord_rows(g.Hs) * 2 : 0},
+        {(void **)&p->bw_rec, p->engine == STKDE_ENGINE_TC ? nrec * sizeof(PointBw) : 0},
+        {(void **)&p->bw_sorted, p->engine == STKDE_ENGINE_TC ? nrec * sizeof(PointBw) : 0},
         {(void **)&p->keys_in, nrec * 4}, {(void **)&p->keys_out, nrec * 4},
         {(void **)&p->vals_in, nrec * 4}, {(void **)&p->vals_out, nrec * 4},
         {(void **)&p->bucket_cnt, ((size_t)p->nbuckets + 1) * 4}, {(void **)&p->bucket_begin, ((size_t)p->nbuckets + 2) * 4},
@@ -250,11 +253,23 @@ static void harvest_timing(stkde_plan_s *p) {
     p->tev_used = 0;
 }
 
+// Per-call state of an adaptive-bandwidth call (p->d_bw), cleared on every exit.
+struct BwScope {
+    stkde_plan_s *p;
+    BwScope(stkde_plan_s *p_, const float *bw) : p(p_) { p->d_bw = bw; }
+    ~BwScope() { p->d_bw = nullptr; }
+};
+
 static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, int64_t n_norm, int64_t t_begin,
-                             int64_t t_end, float *d_out, cudaStream_t st) {
+                             int64_t t_end, float *d_out, cudaStream_t st, const float *d_bw = nullptr) {
     const GridParams &g = p->g;
     p->last_own_launches = 0;
     p->last_cub_calls = 0;
+    if (d_bw && p->engine != STKDE_ENGINE_TC) {
+        set_error("adaptive bandwidths need the tcgen05 engine (H_s <= 120, STKDE_ENGINE unset or 2)");
+        return STKDE_EINVAL;
+    }
+    BwScope scope(p, d_bw);
     if (n < 0 || n_norm < 0) { set_error("n must be >= 0"); return STKDE_EINVAL; }
     if (n > p->max_n) { set_error("n = %lld exceeds the plan's max_n = %lld", (long long)n, (long long)p->max_n); return STKDE_ECAPACITY; }
     if (t_begin < 0 || t_end > g.Gt || t_begin >= t_end) { set_error("slab [t_begin, t_end) must satisfy 0 <= t_begin < t_end <= Gt"); return STKDE_EINVAL; }
@@ -265,9 +280,11 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
         CK(cudaMemsetAsync(d_out, 0, (size_t)g.Gx * g.Gy * Ts * sizeof(float), st));
         return STKDE_OK;
     }
-    // 1/(n hs^2 ht) times the kernel constant (pi/2 or 2/pi).
+    // 1/(n hs^2 ht) times the kernel constant (pi/2 or 2/pi); adaptive
+    // calls: 1/(n sres^2 tres), the tile kernel supplies max_i (sres/hs_i)^2 (tres/ht_i)
     const double kc = p->kernel == STKDE_KERNEL_PRINTED ? M_PI / 2.0 : 2.0 / M_PI;
-    const float cnorm = (float)(kc / ((double)n_norm * (g.hs * g.hs) * g.ht));
+    const float cnorm = d_bw ? (float)(kc / ((double)n_norm * (g.sres * g.sres) * g.tres))
+                             : (float)(kc / ((double)n_norm * (g.hs * g.hs) * g.ht));
     int rc = launch_binning(p, d_points, n, st);
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     if (p->engine == STKDE_ENGINE_TC) {
@@ -295,15 +312,106 @@ extern "C" int stkde_compute_slab(stkde_plan_t p, const float *d_points, int64_t
     return compute_slab_impl(p, d_points, n, n_norm, t_begin, t_end, d_slab, (cudaStream_t)stream);
 }
 
-extern "C" int stkde_count_contributions(stkde_plan_t p, const float *d_points, int64_t n, int64_t t_begin,
-                                         int64_t t_end, int64_t *d_count, void *stream) {
+static int count_impl(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n, int64_t t_begin,
+                      int64_t t_end, int64_t *d_count, void *stream) {
     if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
     if (n < 0 || (n > 0 && !d_points) || !d_count) { set_error("bad points/count arguments"); return STKDE_EINVAL; }
     if (t_begin < 0 || t_end > p->g.Gt || t_begin >= t_end) { set_error("bad slab"); return STKDE_EINVAL; }
     CK(cudaSetDevice(p->device));
-    int rc = launch_count(p, d_points, n, t_begin, t_end, d_count, (cudaStream_t)stream);
+    int rc = launch_count(p, d_points, n, t_begin, t_end, d_count, (cudaStream_t)stream, d_bw);
     if (rc) set_error("count launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return rc;
+}
+
+extern "C" int stkde_count_contributions(stkde_plan_t p, const float *d_points, int64_t n, int64_t t_begin,
+                                         int64_t t_end, int64_t *d_count, void *stream) {
+    return count_impl(p, d_points, nullptr, n, t_begin, t_end, d_count, stream);
+}
+
+extern "C" int stkde_count_contributions_adaptive(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n,
+                                                  int64_t t_begin, int64_t t_end, int64_t *d_count, void *stream) {
+    if (n > 0 && !d_bw) { set_error("d_bw is NULL"); return STKDE_EINVAL; }
+    return count_impl(p, d_points, d_bw, n, t_begin, t_end, d_count, stream);
+}
+
+// ---- adaptive bandwidth (reading R15) ----
+extern "C" int stkde_compute_adaptive(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n,
+                                      float *d_grid, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    if (n > 0 && !d_bw) { set_error("d_bw is NULL"); return STKDE_EINVAL; }
+    return compute_slab_impl(p, d_points, n, n, 0, p->g.Gt, d_grid, (cudaStream_t)stream, n > 0 ? d_bw : nullptr);
+}
+
+extern "C" int stkde_compute_adaptive_slab(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n,
+                                           int64_t n_norm, int64_t t_begin, int64_t t_end, float *d_slab,
+                                           void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    if (n > 0 && !d_bw) { set_error("d_bw is NULL"); return STKDE_EINVAL; }
+    return compute_slab_impl(p, d_points, n, n_norm, t_begin, t_end, d_slab, (cudaStream_t)stream,
+                             n > 0 ? d_bw : nullptr);
+}
+
+// ---- multi-bandwidth sweep (Fig. 1) ----
+// The plan's GridParams narrowed to (hs_k, ht_k) <= (hs, ht): gates, kernel scales and
+// reach (H, Ra, Ray, Rt) of the smaller bandwidth; the home-bucket geometry (tile
+// shape, BTH, key layout) stays the plan's, so one binning serves every bandwidth.
+static GridParams narrowed(const GridParams &g, double hs, double ht) {
+    GridParams k = g;
+    k.hs = hs; k.ht = ht;
+    k.rs = (float)(hs / g.sres);
+    k.rt = (float)(ht / g.tres);
+    k.rs2 = (float)((hs / g.sres) * (hs / g.sres));
+    k.inv_rs = (float)(g.sres / hs);
+    k.inv_rt = (float)(g.tres / ht);
+    k.Hs = (int)std::ceil(hs / g.sres);
+    k.Ht = (int)std::ceil(ht / g.tres);
+    k.Ra = (k.Hs + BX - 1) / BX;
+    k.Ray = (k.Hs + g.BY - 1) / g.BY;
+    k.Rt = (k.Ht + g.BT - 1) / g.BT;
+    return k;
+}
+
+extern "C" int stkde_compute_sweep(stkde_plan_t p, const float *d_points, int64_t n, int nbw, const double *h_hs,
+                                   const double *h_ht, float *const *d_grids, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    if (nbw < 1 || !h_hs || !h_ht || !d_grids) { set_error("bad sweep arguments"); return STKDE_EINVAL; }
+    const GridParams g0 = p->g;
+    for (int k = 0; k < nbw; ++k) {
+        if (!(h_hs[k] > 0) || !(h_ht[k] > 0) || !(h_hs[k] <= g0.hs) || !(h_ht[k] <= g0.ht)) {
+            set_error("sweep bandwidth %d must satisfy 0 < hs_k <= hs and 0 < ht_k <= ht", k);
+            return STKDE_EINVAL;
+        }
+        if (!d_grids[k]) { set_error("d_grids[%d] is NULL", k); return STKDE_EINVAL; }
+    }
+    if (n < 0) { set_error("n must be >= 0"); return STKDE_EINVAL; }
+    if (n > p->max_n) { set_error("n = %lld exceeds the plan's max_n = %lld", (long long)n, (long long)p->max_n); return STKDE_ECAPACITY; }
+    if (n > 0 && !d_points) { set_error("NULL device pointer"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    p->last_own_launches = 0;
+    p->last_cub_calls = 0;
+    const size_t vox = (size_t)g0.Gx * g0.Gy * g0.Gt;
+    if (n == 0) {
+        for (int k = 0; k < nbw; ++k) CK(cudaMemsetAsync(d_grids[k], 0, vox * sizeof(float), st));
+        return STKDE_OK;
+    }
+    int rc = launch_binning(p, d_points, n, st);           // once, at the plan's (largest) reach
+    if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    const double kc = p->kernel == STKDE_KERNEL_PRINTED ? M_PI / 2.0 : 2.0 / M_PI;
+    const int c0 = 0, c1 = g0.NTT;
+    for (int k = 0; k < nbw; ++k) {
+        p->g = narrowed(g0, h_hs[k], h_ht[k]);
+        const float cnorm = (float)(kc / ((double)n * (h_hs[k] * h_hs[k]) * h_ht[k]));
+        if (p->engine == STKDE_ENGINE_TC) rc = launch_chords(p, n, st);
+        if (!rc) rc = launch_worklist(p, c0, c1, st);
+        if (!rc)
+            rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)
+                 : p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)
+                                                    : launch_tile(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st);
+        p->g = g0;
+        if (rc) { set_error("sweep launch %d failed: %s", k, cudaGetErrorString(cudaGetLastError())); return rc; }
+    }
+    return STKDE_OK;
 }
 
 // Cost-balanced Bt-aligned cuts: per-layer cost =
@@ -426,6 +534,7 @@ extern "C" int stkde_plan_check(stkde_plan_t p) {
     CK(cudaMemset(p->counters + 1, 0, sizeof(int)));
     if (flags & 2) { set_error("internal work-list capacity exceeded"); return STKDE_ECUDA; }
     if (flags & 1) { set_error("non-finite point coordinate(s) were skipped"); return STKDE_ENONFINITE; }
+    if (flags & 4) { set_error("point(s) with a bandwidth outside (0, plan hs] x (0, plan ht] were skipped"); return STKDE_EBANDWIDTH; }
     return STKDE_OK;
 }
 
@@ -509,6 +618,7 @@ extern "C" const char *stkde_strerror(int code) {
         case STKDE_ECUDA: return "CUDA error";
         case STKDE_ECAPACITY: return "n exceeds plan capacity (max_n)";
         case STKDE_ENONFINITE: return "non-finite point coordinate";
+        case STKDE_EBANDWIDTH: return "per-point bandwidth outside the plan's range";
     }
     return "unknown error";
 }

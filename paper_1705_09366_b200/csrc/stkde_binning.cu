@@ -49,19 +49,45 @@ __device__ __forceinline__ bool reaches_grid(const GridParams &g, const PointRec
            r.T + g.Ht >= 0 && r.T - g.Ht < g.Gt;
 }
 
-// K1: records, home-tile keys, bucket histogram.
+// Adaptive call: the point's (hs_i, ht_i) must be finite with 0 < hs_i <= hs and
+// 0 < ht_i <= ht (the plan's bandwidths size the binning reach).
+__device__ __forceinline__ bool make_bw(const GridParams &g, const float *__restrict__ bw, int64_t i, PointBw *b) {
+    const float hs = bw[2 * i], ht = bw[2 * i + 1];
+    if (!(hs > 0.f) || !(ht > 0.f) || !((double)hs <= g.hs) || !((double)ht <= g.ht)) return false;
+    b->hs = hs;
+    b->ht = ht;
+    b->inv_rs = (float)(g.sres / (double)hs);
+    b->inv_rt = (float)(g.tres / (double)ht);
+    return true;
+}
+
+// K1: records, home-tile keys, bucket histogram.  Adaptive calls (bw != NULL) also
+// write the per-point bandwidths and the maximum normalisation weight
+// W_i = (sres/hs_i)^2 (tres/ht_i) (as float bits; positive floats order as unsigned).
 __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, PointRec *__restrict__ rec,
                        uint32_t *__restrict__ keys, uint32_t *__restrict__ vals,
-                       uint32_t *__restrict__ bucket_cnt, int *__restrict__ err, uint32_t sentinel) {
+                       uint32_t *__restrict__ bucket_cnt, int *__restrict__ err, uint32_t sentinel,
+                       const float *__restrict__ bw, PointBw *__restrict__ bw_rec, unsigned *__restrict__ wmax) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float x = pts[3 * i], y = pts[3 * i + 1], t = pts[3 * i + 2];
     PointRec r;
     uint32_t key = sentinel;
+    bool bw_ok = true;
+    if (bw) {
+        PointBw b{0.f, 0.f, 0.f, 0.f};
+        bw_ok = make_bw(g, bw, i, &b);
+        if (!bw_ok) atomicOr(err, 4);
+        else {
+            const double ws = g.sres / (double)b.hs, wt = g.tres / (double)b.ht;
+            atomicMax(wmax, __float_as_uint((float)(ws * ws * wt)));
+        }
+        bw_rec[i] = b;
+    }
     if (!make_rec(g, x, y, t, &r)) {
         atomicOr(err, 1);
         r = PointRec{0, 0, 0, 0.f, 0.f, 0.f, 0.f, 0.f};
-    } else if (reaches_grid(g, r)) {
+    } else if (bw_ok && reaches_grid(g, r)) {
         int a = min(max(r.X, 0), g.Gx - 1) / BX;
         int b = min(max(r.Y, 0), g.Gy - 1) / g.BY;
         int c = min(max(r.T, 0), g.Gt - 1) / g.BTH;
@@ -73,11 +99,17 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
     vals[i] = (uint32_t)i;
 }
 
-// K1b: records in bucket order (coalesced candidate reads in the tile kernel).
+// K1b: records (and adaptive bandwidths) in bucket order (coalesced candidate reads
+// in the tile kernel).
 __global__ void k_permute(const PointRec *__restrict__ rec, const uint32_t *__restrict__ vals,
-                          PointRec *__restrict__ out, int64_t n) {
+                          PointRec *__restrict__ out, int64_t n, const PointBw *__restrict__ bw_rec,
+                          PointBw *__restrict__ bw_out) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < n) out[j] = rec[vals[j]];
+    if (j < n) {
+        const uint32_t v = vals[j];
+        out[j] = rec[v];
+        if (bw_rec) bw_out[j] = bw_rec[v];
+    }
 }
 
 // Exact disc chords of every (sorted) point, for the tcgen05 engine.  Point i
@@ -86,14 +118,17 @@ __global__ void k_permute(const PointRec *__restrict__ rec, const uint32_t *__re
 // one aligned 16-byte block.  Entry = int8 (lo, hi): columns [X_i + lo,
 // X_i + hi] whose centres pass the spatial gate of Alg. 1,
 // (1, 0) for an empty row; computed once per point instead of once per
-// (point, tile) visit.  Requires H_s <= 120.
-__global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams g, uint16_t *__restrict__ chords) {
-    const int rows = chord_rows(g.Hs);
+// (point, tile) visit.  Requires H_s <= 120.  Adaptive calls (bw != NULL): the
+// disc of point i has its own radius hs_i (the table layout keeps the plan's H_s).
+__global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams gp, uint16_t *__restrict__ chords,
+                         const PointBw *__restrict__ bw) {
+    const int rows = chord_rows(gp.Hs);
     const int64_t total = n * rows;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / rows;
         const int j = (int)(e - i * rows);
         const PointRec r = rec[i];
+        const GridParams g = bw ? with_point_bw(gp, bw[i]) : gp;
         const int Y = ((r.Y - g.Hs) & ~7) + j;
         int dl = 1, dh = 0;
         if (Y >= r.Y - g.Hs && Y <= r.Y + g.Hs) {
@@ -180,16 +215,19 @@ __global__ void k_items(const uint32_t *__restrict__ lval, const uint64_t *__res
         items[i0 + j] = make_int4((int)lval[k], (int)j, (int)nch, nch > 1 ? (int)s0 : -1);
 }
 
-// Exact contribution count: one warp per point.
-__global__ void k_count(const float *__restrict__ pts, int64_t n, GridParams g, int64_t t_begin, int64_t t_end,
-                        unsigned long long *__restrict__ out) {
+// Exact contribution count: one warp per point (adaptive: the point's own bandwidths).
+__global__ void k_count(const float *__restrict__ pts, int64_t n, GridParams gp, int64_t t_begin, int64_t t_end,
+                        unsigned long long *__restrict__ out, const float *__restrict__ bwin) {
     __shared__ unsigned long long part[32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     unsigned long long mine = 0;
     if (i < n) {
         PointRec r;
-        if (make_rec(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], &r) && reaches_grid(g, r)) {
+        PointBw b{0.f, 0.f, 0.f, 0.f};
+        const bool bw_ok = !bwin || make_bw(gp, bwin, i, &b);
+        const GridParams g = bwin ? with_point_bw(gp, b) : gp;
+        if (bw_ok && make_rec(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], &r) && reaches_grid(gp, r)) {
             int cols = 0, lay = 0;
             int y0 = max(r.Y - g.Hs, 0), y1 = min(r.Y + g.Hs, g.Gy - 1);
             for (int Y = y0 + lane; Y <= y1; Y += 32) {
@@ -245,13 +283,17 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st) {
     const GridParams &g = p->g;
     cudaMemsetAsync(p->bucket_cnt, 0, (p->nbuckets + 1) * sizeof(uint32_t), st);
+    const bool ad = p->d_bw != nullptr;
+    if (ad) cudaMemsetAsync(p->counters + 6, 0, sizeof(int), st);
     k_prep<<<nblk(n, 256), 256, 0, st>>>(d_points, n, g, p->rec, p->keys_in, p->vals_in, p->bucket_cnt,
-                                          p->counters + 1, (uint32_t)p->nbuckets);
+                                          p->counters + 1, (uint32_t)p->nbuckets, p->d_bw,
+                                          ad ? p->bw_rec : nullptr, reinterpret_cast<unsigned *>(p->counters + 6));
     size_t bytes = p->cub_bytes;
     if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->keys_in, p->keys_out, p->vals_in, p->vals_out,
                                         (int)n, 0, p->key_bits, st) != cudaSuccess)
         return STKDE_ECUDA;
-    k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n);
+    k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n, ad ? p->bw_rec : nullptr,
+                                             p->bw_sorted);
     bytes = p->cub_bytes;
     if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->bucket_cnt, p->bucket_begin, (int)(p->nbuckets + 1), st) !=
         cudaSuccess)
@@ -265,7 +307,7 @@ int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
     const int64_t total = n * chord_rows(p->g.Hs);
     if (total > 0) {
         const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 16);
-        k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords);
+        k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr);
         p->last_own_launches += 1;
     }
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
@@ -291,11 +333,11 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
 }
 
 int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_begin, int64_t t_end,
-                 int64_t *d_count, cudaStream_t st) {
+                 int64_t *d_count, cudaStream_t st, const float *d_bw) {
     cudaMemsetAsync(d_count, 0, sizeof(int64_t), st);
     if (n > 0)
         k_count<<<nblk(n * 32, 256), 256, 0, st>>>(d_points, n, p->g, t_begin, t_end,
-                                                   reinterpret_cast<unsigned long long *>(d_count));
+                                                   reinterpret_cast<unsigned long long *>(d_count), d_bw);
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }
 

@@ -37,6 +37,14 @@ struct __align__(16) PointRec {
     float x, y;
 };
 
+// Per-point bandwidths of the adaptive estimator (reading R15), one per
+// record: hs_i, ht_i as given (world units, exact FP64 gates) and the voxel-unit
+// reciprocals sres/hs_i, tres/ht_i of the FP32 tables.
+struct __align__(16) PointBw {
+    float hs, ht;
+    float inv_rs, inv_rt;
+};
+
 // Kernel-side view of a plan (passed by value).
 struct GridParams {
     double x0, y0, t0;      // origin (world)
@@ -57,6 +65,21 @@ struct GridParams {
 // rows of a point's chord table (tcgen05 engine): the 8-aligned row blocks that
 // cover [Y_i - H_s, Y_i + H_s] for any Y_i
 __host__ __device__ inline int chord_rows(int Hs) { return ((2 * Hs + 1 + 7) / 8 + 1) * 8; }
+
+// The plan's GridParams with the spatial bandwidth of one point (adaptive chords,
+// gates and counts): everything the exact gates read, nothing the binning reads.
+__host__ __device__ inline GridParams with_point_bw(const GridParams &g, const PointBw &b) {
+    GridParams gi = g;
+    gi.hs = (double)b.hs;
+    gi.ht = (double)b.ht;
+    const double rs = (double)b.hs / g.sres;
+    gi.rs = (float)rs;
+    gi.rs2 = (float)(rs * rs);
+    gi.rt = (float)((double)b.ht / g.tres);
+    gi.inv_rs = b.inv_rs;
+    gi.inv_rt = b.inv_rt;
+    return gi;
+}
 
 __host__ __device__ inline int floordiv(int a, int b) {
     int q = a / b;
@@ -169,6 +192,8 @@ struct stkde_plan_s {
     size_t ws_bytes;
     stkde::PointRec *rec, *rec_sorted;
     uint16_t *chords;           // tcgen05 engine: [max_n][chord_rows(Hs)] exact disc chords (int8 lo, hi - X_i)
+    stkde::PointBw *bw_rec, *bw_sorted;   // tcgen05 engine: per-point bandwidths of an adaptive call
+    const float *d_bw;          // the current call's per-point bandwidths [n][2] (NULL: fixed bandwidth)
     uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
     uint32_t *bucket_cnt;       // [ntiles + 1]
     uint32_t *bucket_begin;     // [ntiles + 2]
@@ -179,6 +204,7 @@ struct stkde_plan_s {
     float *partials;            // [max_slots][256*BT]
     int *counters;              // [0] work counter, [1] error flag, [2..3] u64 issued MMA columns,
                                 // [4..5] u64 issued k-blocks (tcgen05 engine instrumentation),
+                                // [6] adaptive call: max_i (sres/hs_i)^2 (tres/ht_i) as float bits,
                                 // [32..95] u64 [32] tcgen05 phase profile (stkde_plan_tc_profile)
     int tc_profile;             // STKDE_TC_PROF: record the tcgen05 kernel's phase profile
     int tc_watchdog;            // STKDE_TC_WATCHDOG: bounded mbarrier waits, record in counters[96..97]
@@ -204,7 +230,7 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,
                 float *out, cudaStream_t st);
 int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_begin,
-                 int64_t t_end, int64_t *d_count, cudaStream_t st);
+                 int64_t t_end, int64_t *d_count, cudaStream_t st, const float *d_bw = nullptr);
 int launch_hist_t(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
 int launch_gather(const float *slab, int64_t Gx, int64_t Gy, int64_t Gt, int64_t t0, int64_t t1,
                   float *full, cudaStream_t st);

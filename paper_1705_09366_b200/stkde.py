@@ -17,6 +17,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libstkde.so")
 
 STKDE_OK, STKDE_EINVAL, STKDE_ENOMEM, STKDE_ECUDA, STKDE_ECAPACITY, STKDE_ENONFINITE = 0, -1, -2, -3, -4, -5
+STKDE_EBANDWIDTH = -6
 KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
 
 # Exported entry points of include/stkde.h (checked by tests/test_abi.py).
@@ -24,7 +25,8 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
            "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress", "stkde_strerror",
-           "stkde_last_error")
+           "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
+           "stkde_count_contributions_adaptive", "stkde_compute_sweep")
 
 
 class StkdeError(RuntimeError):
@@ -73,6 +75,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_mma_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.stkde_plan_tc_profile.argtypes = [P, ctypes.POINTER(ctypes.c_uint64)]
     L.stkde_plan_debug_progress.argtypes = [P, P]
+    L.stkde_compute_adaptive.argtypes = [P, P, P, I64, P, P]
+    L.stkde_compute_adaptive_slab.argtypes = [P, P, P, I64, I64, I64, I64, P, P]
+    L.stkde_count_contributions_adaptive.argtypes = [P, P, P, I64, I64, I64, P, P]
+    L.stkde_compute_sweep.argtypes = [P, P, I64, I32, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(P), P]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
@@ -80,7 +86,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition", "stkde_slab_cuts",
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
-                 "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress"):
+                 "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress",
+                 "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
+                 "stkde_compute_sweep"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -104,6 +112,14 @@ def _points_arg(points: torch.Tensor, device: torch.device) -> torch.Tensor:
     if points.dtype != torch.float32 or points.dim() != 2 or points.shape[1] != 3:
         raise ValueError("points must be float32 [n, 3] (x, y, t)")
     return points.contiguous()
+
+
+def _bw_arg(bw: torch.Tensor, device: torch.device, n: int) -> torch.Tensor:
+    if not isinstance(bw, torch.Tensor) or bw.device != device:
+        raise ValueError("bw must be a CUDA tensor on %s" % device)
+    if bw.dtype != torch.float32 or bw.dim() != 2 or bw.shape[1] != 2 or bw.shape[0] != n:
+        raise ValueError("bw must be float32 [n, 2] (hs_i, ht_i)")
+    return bw.contiguous()
 
 
 class Plan:
@@ -173,6 +189,65 @@ class Plan:
         _check(load_library().stkde_compute_slab(self._h, pts.data_ptr(), pts.shape[0], nn, int(t_begin),
                                                  int(t_end), out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
+
+    # -- adaptive bandwidth (include/stkde.h; reading R15) --
+    def compute_adaptive(self, points: torch.Tensor, bw: torch.Tensor, out: Optional[torch.Tensor] = None,
+                         stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Full grid with per-point bandwidths bw = float32 [n, 2] (hs_i, ht_i) <= the plan's."""
+        pts = _points_arg(points, self.device)
+        b = _bw_arg(bw, self.device, pts.shape[0])
+        if out is None:
+            out = torch.empty(self.G, dtype=torch.float32, device=self.device)
+        self._check_out(out, self.G[2])
+        _check(load_library().stkde_compute_adaptive(self._h, pts.data_ptr(), b.data_ptr(), pts.shape[0],
+                                                      out.data_ptr(), _stream_ptr(stream, self.device)))
+        return out
+
+    def compute_adaptive_slab(self, points: torch.Tensor, bw: torch.Tensor, t_begin: int, t_end: int,
+                              n_norm: Optional[int] = None, out: Optional[torch.Tensor] = None,
+                              stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        pts = _points_arg(points, self.device)
+        b = _bw_arg(bw, self.device, pts.shape[0])
+        ts = int(t_end) - int(t_begin)
+        if out is None:
+            out = torch.empty((self.G[0], self.G[1], max(ts, 0)), dtype=torch.float32, device=self.device)
+        self._check_out(out, ts)
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        _check(load_library().stkde_compute_adaptive_slab(self._h, pts.data_ptr(), b.data_ptr(), pts.shape[0], nn,
+                                                           int(t_begin), int(t_end), out.data_ptr(),
+                                                           _stream_ptr(stream, self.device)))
+        return out
+
+    def count_contributions_adaptive(self, points: torch.Tensor, bw: torch.Tensor, t_begin: int = 0,
+                                     t_end: Optional[int] = None,
+                                     stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        pts = _points_arg(points, self.device)
+        b = _bw_arg(bw, self.device, pts.shape[0])
+        out = torch.empty(1, dtype=torch.int64, device=self.device)
+        _check(load_library().stkde_count_contributions_adaptive(
+            self._h, pts.data_ptr(), b.data_ptr(), pts.shape[0], int(t_begin),
+            int(self.G[2] if t_end is None else t_end), out.data_ptr(), _stream_ptr(stream, self.device)))
+        return out
+
+    # -- multi-bandwidth sweep (include/stkde.h) --
+    def compute_sweep(self, points: torch.Tensor, hs: Sequence[float], ht: Sequence[float],
+                      outs: Optional[Sequence[torch.Tensor]] = None,
+                      stream: Optional[torch.cuda.Stream] = None) -> list:
+        """One binning, len(hs) grids: grid k at bandwidths (hs[k], ht[k]) <= the plan's."""
+        pts = _points_arg(points, self.device)
+        k = len(hs)
+        if len(ht) != k or k < 1:
+            raise ValueError("hs and ht must be equally long, non-empty")
+        if outs is None:
+            outs = [torch.empty(self.G, dtype=torch.float32, device=self.device) for _ in range(k)]
+        for o in outs:
+            self._check_out(o, self.G[2])
+        H = (ctypes.c_double * k)(*[float(v) for v in hs])
+        T = (ctypes.c_double * k)(*[float(v) for v in ht])
+        ptrs = (ctypes.c_void_p * k)(*[o.data_ptr() for o in outs])
+        _check(load_library().stkde_compute_sweep(self._h, pts.data_ptr(), pts.shape[0], k, H, T, ptrs,
+                                                  _stream_ptr(stream, self.device)))
+        return list(outs)
 
     def _check_out(self, out, ts):
         if out.device != self.device or out.dtype != torch.float32 or not out.is_contiguous() \
