@@ -19,6 +19,14 @@ the grid (slab) comes back D2H, both inside the timed region.
 
 --impl reference: the FP64 CPU oracle (oracle/) timed on this host's cores on
 a bounded sample of the same workload (rank 0 only; other ranks exit 0).
+
+--variant (default `fixed` is the driver's headline):
+  adaptive  per-point bandwidths (stkde_compute_adaptive_slab) from
+            stkde_synth.adaptive_bandwidths (Abramson square-root law on a pilot
+            histogram, lambda in [0.25, 1]); C = the adaptive gated pairs.
+  sweep     stkde_compute_sweep over (f hs, f ht), f in stkde_synth.SWEEP_FRACTIONS:
+            one binning, one grid per bandwidth; C = sum over the grids.  N = 1 only.
+            `separate_ms` times the same grids as separate plans + computes.
 """
 import argparse
 import json
@@ -126,28 +134,43 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- reference ---
-def run_oracle_sample(w, m):
+def run_oracle_sample(w, m, variant="fixed"):
+    """The oracle as it stands on the first m points: (contributions, seconds)."""
     import oracle
     oracle.build()
     g = w.grid_kwargs()
     pts = np.ascontiguousarray(w.points[:m])
     t0 = time.perf_counter()
-    r = oracle.stkde_pb(pts, with_ambiguity=False, nthreads=host_cores(), **g)
+    if variant == "adaptive":
+        bw = synth.adaptive_bandwidths(w)[:m]
+        r = oracle.stkde_pb_adaptive(pts, bw, with_ambiguity=False, nthreads=host_cores(), **g)
+        C = r.contributions
+    elif variant == "sweep":
+        C = 0
+        for f in synth.SWEEP_FRACTIONS:
+            r = oracle.stkde_pb(pts, with_ambiguity=False, nthreads=host_cores(),
+                                **dict(g, hs=f * w.hs, ht=f * w.ht))
+            C += r.contributions
+    else:
+        r = oracle.stkde_pb(pts, with_ambiguity=False, nthreads=host_cores(), **g)
+        C = r.contributions
     dt = time.perf_counter() - t0
-    return r.contributions, dt
+    return C, dt
 
 
 def reference_main(args, w, rank):
     if rank != 0:
         return 0
     m = min(REF_SAMPLE[w.name], w.n)
-    sample = "first %d of %d points of the %s workload, full %dx%dx%d grid (FP64 oracle, PB form)" % (
-        m, w.n, w.name, *w.G)
+    if args.variant == "sweep":
+        m = max(m // len(synth.SWEEP_FRACTIONS), 1)
+    sample = "first %d of %d points of the %s workload, full %dx%dx%d grid (FP64 oracle, PB form%s)" % (
+        m, w.n, w.name, *w.G, "" if args.variant == "fixed" else ", " + args.variant)
     if args.warmup > 0:
-        run_oracle_sample(w, min(m, 500))
+        run_oracle_sample(w, min(m, 500), args.variant)
     vals, secs = [], []
     for _ in range(max(args.steps, 1)):
-        C, dt = run_oracle_sample(w, m)
+        C, dt = run_oracle_sample(w, m, args.variant)
         vals.append(C / dt)
         secs.append(dt)
     v = statistics.median(vals)
@@ -155,11 +178,19 @@ def reference_main(args, w, rank):
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": config_dict(w, None),
+           "data": "synthetic", "config": config_dict(w, None, variant_config(args.variant)),
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}}
     print(json.dumps(out))
     return 0
+
+
+def variant_config(variant):
+    if variant == "adaptive":
+        return {"variant": "adaptive bandwidth (DESIGN.md R15): stkde_synth.adaptive_bandwidths, lambda in [0.25, 1]"}
+    if variant == "sweep":
+        return {"variant": "multi-bandwidth sweep: (f hs, f ht), f in %s, one binning" % (list(synth.SWEEP_FRACTIONS),)}
+    return {}
 
 
 def config_dict(w, info, extra=None):
@@ -185,24 +216,54 @@ def gpu_main(args, w, rank, world, local_rank):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     g = w.grid_kwargs()
+    variant = args.variant
+    if variant == "sweep" and world > 1:
+        if rank == 0:
+            print(json.dumps({"variant": "sweep", "unavailable": "the sweep bench runs on one GPU"}))
+        dist.destroy_process_group()
+        return 0
     stream = torch.cuda.Stream(dev)
     plan = S.Plan(max_n=w.n, device=local_rank, **g)
     info = plan.info()
     pts = torch.from_numpy(w.points).to(dev)
+    bw_host = synth.adaptive_bandwidths(w) if variant == "adaptive" else None
+    bw = torch.from_numpy(bw_host).to(dev) if bw_host is not None else None
+    fr = synth.SWEEP_FRACTIONS
+    sw_hs, sw_ht = [f * w.hs for f in fr], [f * w.ht for f in fr]
     with torch.cuda.stream(stream):
         cuts = plan.slab_partition(pts, world, stream=stream) if world > 1 else [0, w.G[2]]
         t0, t1 = cuts[rank], cuts[rank + 1]
-        C = int(plan.count_contributions(pts, t0, t1, stream=stream).item()) if t1 > t0 else 0
+        if t1 <= t0:
+            C = 0
+        elif variant == "adaptive":
+            C = int(plan.count_contributions_adaptive(pts, bw, t0, t1, stream=stream).item())
+        elif variant == "sweep":
+            C = 0
+            for hs_k, ht_k in zip(sw_hs, sw_ht):
+                with S.Plan(max_n=w.n, device=local_rank, **dict(g, hs=hs_k, ht=ht_k)) as q:
+                    C += int(q.count_contributions(pts, t0, t1, stream=stream).item())
+        else:
+            C = int(plan.count_contributions(pts, t0, t1, stream=stream).item())
     Ct = torch.tensor([C], dtype=torch.int64, device=dev)
     if world > 1:
         dist.all_reduce(Ct)
     C_total = int(Ct.item())
     out = torch.empty((w.G[0], w.G[1], max(t1 - t0, 1)), dtype=torch.float32, device=dev)
+    outs = [out] + [torch.empty_like(out) for _ in fr[1:]] if variant == "sweep" else [out]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
+    def run(p_pts, p_bw):
+        if t1 <= t0:
+            return
+        if variant == "adaptive":
+            plan.compute_adaptive_slab(p_pts, p_bw, t0, t1, n_norm=w.n, out=out, stream=stream)
+        elif variant == "sweep":
+            plan.compute_sweep(p_pts, sw_hs, sw_ht, outs=outs, stream=stream)
+        else:
+            plan.compute_slab(p_pts, t0, t1, n_norm=w.n, out=out, stream=stream)
+
     def step():
-        if t1 > t0:
-            plan.compute_slab(pts, t0, t1, n_norm=w.n, out=out, stream=stream)
+        run(pts, bw)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -237,7 +298,7 @@ def gpu_main(args, w, rank, world, local_rank):
     plan.enable_kernel_timing(False)
     mma_cols, mma_kblocks = plan.mma_stats()
     ms = sum(ms_steps) / len(ms_steps)
-    kernel_ms = kms / max(klaunch, 1)
+    kernel_ms = kms / max(args.steps, 1)          # tile-kernel time per step (all its launches)
     vals = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vals, op=dist.ReduceOp.MAX)
@@ -245,7 +306,8 @@ def gpu_main(args, w, rank, world, local_rank):
 
     # ---- e2e through the public API: pinned host points in, grid (slab) out ----
     host_pts = torch.from_numpy(w.points).pin_memory()
-    host_out = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory()
+    host_bw = torch.from_numpy(bw_host).pin_memory() if bw_host is not None else None
+    host_outs = [torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory() for _ in outs]
     e2e_steps = max(1, min(args.steps, 10))
     barrier()
     eb, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -253,21 +315,46 @@ def gpu_main(args, w, rank, world, local_rank):
         eb.record(stream)
         for _ in range(e2e_steps):
             dpts = host_pts.to(dev, non_blocking=True)
-            if t1 > t0:
-                plan.compute_slab(dpts, t0, t1, n_norm=w.n, out=out, stream=stream)
-            host_out.copy_(out, non_blocking=True)
+            dbw = host_bw.to(dev, non_blocking=True) if host_bw is not None else None
+            run(dpts, dbw)
+            for ho, o in zip(host_outs, outs):
+                ho.copy_(o, non_blocking=True)
         ee.record(stream)
     barrier()
     e2e_ms = torch.tensor([eb.elapsed_time(ee) / e2e_steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
-    h2d = w.points.nbytes * world
-    d2h = w.G[0] * w.G[1] * w.G[2] * 4
+    h2d = (w.points.nbytes + (bw_host.nbytes if bw_host is not None else 0)) * world
+    d2h = w.G[0] * w.G[1] * w.G[2] * 4 * len(outs)
+
+    # sweep: the same grids as separate plans + computes (what the one binning saves)
+    separate_ms = None
+    if variant == "sweep":
+        qs = [S.Plan(max_n=w.n, device=local_rank, **dict(g, hs=a, ht=b)) for a, b in zip(sw_hs, sw_ht)]
+        def sep():
+            for q, o in zip(qs, outs):
+                q.compute(pts, out=o, stream=stream)
+        with torch.cuda.stream(stream):
+            for _ in range(args.warmup):
+                sep()
+        barrier()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(max(1, min(args.steps, 10)))]
+        with torch.cuda.stream(stream):
+            for a, b in evs:
+                flush.fill_(1)
+                a.record(stream)
+                sep()
+                b.record(stream)
+        barrier()
+        separate_ms = sum(a.elapsed_time(b) for a, b in evs) / len(evs)
+        for q in qs:
+            q.close()
 
     # ---- roofline of the dominant kernel (the tile kernel) ----
     (hbm_peak, hbm_src), (bf16_peak, bf16_src) = peaks()
-    grid_bytes = w.G[0] * w.G[1] * (t1 - t0) * 4
+    grid_bytes = w.G[0] * w.G[1] * (t1 - t0) * 4 * len(outs)
     t_fp32 = 2.0 * C / (FP32_NOMINAL_TFLOPS * 1e12)
     t_hbm = grid_bytes / (hbm_peak * 1e9)
     if t_fp32 >= t_hbm:
@@ -280,7 +367,7 @@ def gpu_main(args, w, rank, world, local_rank):
         ach = grid_bytes / (kernel_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                 "peak_source": hbm_src}
-    roof["traffic"] = profile_traffic(w.name, info["engine"])
+    roof["traffic"] = profile_traffic(w.name, info["engine"], variant)
     roof["kernel"] = KERNELS[info["engine"]] % info["Bt"]
     roof["kernel_ms"] = kernel_ms_max
     roof["algorithmic"] = {"flops": 2 * C, "bytes": grid_bytes,
@@ -305,18 +392,21 @@ def gpu_main(args, w, rank, world, local_rank):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             m = min(ORACLE_SAMPLE[w.name], w.n)
-            Cs, dt = run_oracle_sample(w, m)
+            if variant == "sweep":
+                m = max(m // len(fr), 1)
+            Cs, dt = run_oracle_sample(w, m, variant)
             cpu = {"value": Cs / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
-                   "sample": "first %d of %d points, full %dx%dx%d grid, FP64 oracle (PB form), %.1f s"
-                             % (m, w.n, *w.G, dt)}
+                   "sample": "first %d of %d points, full %dx%dx%d grid, FP64 oracle (PB form%s), %.1f s"
+                             % (m, w.n, *w.G, "" if variant == "fixed" else ", " + variant, dt)}
         result = {
             "metric": METRIC, "value": C_total / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": config_dict(w, info, {"contributions": C_total, "ms_per_grid": ms_max,
-                                            "parallelism": "time-slab x%d" % world, "slab_cuts": cuts,
-                                            "l2": "flushed between timed steps (256 MiB write, untimed)",
-                                            "inputs_resident": True}),
+            "config": config_dict(w, info, dict(variant_config(variant), **{
+                "contributions": C_total, "ms_per_grid": ms_max / len(outs),
+                "parallelism": "time-slab x%d" % world, "slab_cuts": cuts,
+                "l2": "flushed between timed steps (256 MiB write, untimed)",
+                "inputs_resident": True})),
             "e2e": {"value": C_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
             "gpu_launches": own * args.steps,
@@ -327,6 +417,10 @@ def gpu_main(args, w, rank, world, local_rank):
             "engine": ENGINES[info["engine"]],
             "cpu_baseline": cpu,
         }
+        if variant != "fixed":
+            result["variant"] = variant
+        if separate_ms is not None:
+            result["separate_ms"] = separate_ms
         print(json.dumps(result))
     plan.close()
     if world > 1:
@@ -334,13 +428,14 @@ def gpu_main(args, w, rank, world, local_rank):
     return 0
 
 
-def profile_traffic(name, engine):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the tile kernel from the
+def profile_traffic(name, engine, variant="fixed"):
+    """dram__bytes_read.sum + dram__bytes_write.sum per step of the tile kernel from the
     committed ncu --set full capture of this workload and engine (profiles/traffic.json)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("%s/engine%d" % (name, engine))
+            key = "%s/engine%d" % (name, engine) + ("" if variant == "fixed" else "/" + variant)
+            return json.load(open(p)).get(key)
         except Exception:
             return None
     return None
@@ -354,6 +449,7 @@ def main():
     ap.add_argument("--config", default="stress", choices=sorted(CONFIG_INDEX))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--variant", default="fixed", choices=["fixed", "adaptive", "sweep"])
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

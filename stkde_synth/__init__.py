@@ -253,3 +253,35 @@ def make_config(name: str) -> Workload:
 
 def points_sha256(points: np.ndarray) -> str:
     return hashlib.sha256(np.ascontiguousarray(points, dtype=np.float32).tobytes()).hexdigest()
+
+
+def adaptive_bandwidths(w: Workload, lo: float = 0.25) -> np.ndarray:
+    """Per-point bandwidths float32 [n, 2] = (hs_i, ht_i) for the adaptive estimator
+    (reading R15): a synthetic input recipe, not the
+    method.  Abramson's square-root law on a pilot density: rho_i = count of the
+    coarse (hs x hs x ht) histogram cell holding point i, lambda_i =
+    (rho_i / geometric mean rho)^(-1/2) clamped to [lo, 1], (hs_i, ht_i) =
+    lambda_i (hs, ht) -- dense clusters get narrow kernels, sparse background the
+    plan's.  Every value is <= the plan's (hs, ht) in FP32 (largest float32 <= h)."""
+    p = w.points.astype(np.float64)
+    o = np.array(w.origin, np.float64)
+    cell = np.array([w.hs, w.hs, w.ht], np.float64)
+    nb = np.maximum(np.ceil(np.array(w.G, np.float64) * np.array([w.sres, w.sres, w.tres]) / cell), 1).astype(np.int64)
+    idx = np.clip(np.floor((p - o) / cell).astype(np.int64), 0, nb - 1)
+    flat = (idx[:, 0] * nb[1] + idx[:, 1]) * nb[2] + idx[:, 2]
+    cnt = np.bincount(flat, minlength=int(nb.prod()))[flat].astype(np.float64)
+    g = np.exp(np.mean(np.log(cnt)))
+    lam = np.clip((cnt / g) ** -0.5, lo, 1.0)
+
+    def cap(h):
+        c = np.float32(h)
+        return c if float(c) <= h else np.nextafter(c, np.float32(0))
+    bw = np.empty((len(p), 2), np.float32)
+    bw[:, 0] = np.minimum((lam * w.hs).astype(np.float32), cap(w.hs))
+    bw[:, 1] = np.minimum((lam * w.ht).astype(np.float32), cap(w.ht))
+    return bw
+
+
+# The multi-bandwidth sweep of the bench (SURVEY §8(f) row 4): the plan's bandwidth
+# and three narrower ones (the paper's Lb / Hb / VHb instance ladder, PAPER.md:651-653).
+SWEEP_FRACTIONS = (1.0, 0.75, 0.5, 0.25)
