@@ -225,3 +225,46 @@ def test_sweep_rejects_wider_bandwidth(S):
     with S.Plan(max_n=50, device=0, **g) as p:
         with pytest.raises(S.StkdeError):
             p.compute_sweep(torch.from_numpy(pts).to(dev), [3.5], [2.0])
+
+
+# ------------------------------------------- full sizes (bench.py --variant) ---
+def _sample_voxels(gpu, rng, k_top=600, k_rand=600):
+    flat = gpu.reshape(-1)
+    top = np.argpartition(flat, -k_top)[-k_top:]
+    nz = np.flatnonzero(flat > 0)
+    pick = nz[(rng.uniform01(k_rand) * len(nz)).astype(np.int64) % len(nz)]
+    rnd = (rng.uniform01(200) * flat.size).astype(np.int64) % flat.size
+    return np.unique(np.concatenate([top, pick, rnd]))
+
+
+@pytest.mark.parametrize("name", ["social", "stress"])
+def test_adaptive_full_size_sampled(S, oracle_mod, name):
+    # the bench's adaptive workload (stkde_synth.adaptive_bandwidths) at the
+    # BASELINE.json size: sampled voxels against adaptive Alg. 1, exact C
+    w = synth.make_config(name)
+    g = w.grid_kwargs()
+    bw = synth.adaptive_bandwidths(w)
+    gpu, C, _ = run_adaptive(S, w.points, bw, **g)
+    vox = _sample_voxels(gpu, synth.SplitMix64(13))
+    val, slack, amb = oracle_mod.stkde_vb_voxels_adaptive(w.points, bw, vox, **g)
+    assert_parity(gpu.reshape(-1)[vox], val, slack, amb, vmax=max(val.max(), 0.0), what=name + "/adaptive")
+    assert C == oracle_mod.contributions_adaptive(w.points, bw, **g)
+
+
+def test_sweep_full_size_sampled(S, oracle_mod):
+    # the bench's sweep (stress, f = 1 .. 0.25) at full size, sampled per grid
+    w = synth.make_config("stress")
+    g = w.grid_kwargs()
+    dev = torch.device("cuda", 0)
+    fr = synth.SWEEP_FRACTIONS
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        outs = p.compute_sweep(torch.from_numpy(w.points).to(dev), [f * w.hs for f in fr], [f * w.ht for f in fr])
+        torch.cuda.synchronize()
+        p.check()
+        grids = [o.cpu().numpy() for o in outs]
+        del outs
+    for k, (f, gpu) in enumerate(zip(fr, grids)):
+        gk = dict(g, hs=f * w.hs, ht=f * w.ht)
+        vox = _sample_voxels(gpu, synth.SplitMix64(17 + k), k_top=300, k_rand=300)
+        val, slack, amb = oracle_mod.stkde_vb_voxels(w.points, vox, **gk)
+        assert_parity(gpu.reshape(-1)[vox], val, slack, amb, vmax=max(val.max(), 0.0), what="sweep f=%g" % f)
