@@ -224,6 +224,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     CK(cudaMemset(p->counters, 0, 128 * 4));
     p->tc_profile = env_int("STKDE_TC_PROF", 0);
     p->tc_watchdog = env_int("STKDE_TC_WATCHDOG", 0);
+    p->no_tma = env_int("STKDE_NO_TMA", 0);
     *out = p;
     return STKDE_OK;
 }

@@ -208,6 +208,7 @@ struct stkde_plan_s {
                                 // [32..95] u64 [32] tcgen05 phase profile (stkde_plan_tc_profile)
     int tc_profile;             // STKDE_TC_PROF: record the tcgen05 kernel's phase profile
     int tc_watchdog;            // STKDE_TC_WATCHDOG: bounded mbarrier waits, record in counters[96..97]
+    int no_tma;                 // STKDE_NO_TMA: epilogue stores by per-column bulk copies instead of TMA
     void *debug_progress;       // stkde_plan_debug_progress: per-(CTA, warp) protocol state (host-mapped)
     int *hist_t;                // [Gt + 1] slab-partition histogram
     void *cub_tmp;
