@@ -124,9 +124,18 @@ __global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams
                          const PointBw *__restrict__ bw) {
     const int rows = chord_rows(gp.Hs);
     const int64_t total = n * rows;
+    const bool small = total < ((int64_t)1 << 31);   // 32-bit index division (the 64-bit one is ~4x dearer)
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / rows;
-        const int j = (int)(e - i * rows);
+        int64_t i;
+        int j;
+        if (small) {
+            const uint32_t e32 = (uint32_t)e, i32 = e32 / (uint32_t)rows;
+            i = i32;
+            j = (int)(e32 - i32 * (uint32_t)rows);
+        } else {
+            i = e / rows;
+            j = (int)(e - i * rows);
+        }
         const PointRec r = rec[i];
         const GridParams g = bw ? with_point_bw(gp, bw[i]) : gp;
         const int Y = ((r.Y - g.Hs) & ~7) + j;
