@@ -43,3 +43,31 @@ def test_config_frozen_and_in_box(name):
 def test_ornith_frozen():
     w = synth.make_config("ornith")
     assert synth.points_sha256(w.points) == GOLD["ornith"]["sha256"]
+
+
+@pytest.mark.parametrize("name", ["dengue", "social", "stress"])
+def test_adaptive_bandwidths_recipe(name):
+    # the bench's adaptive-variant inputs: float32 [n, 2], inside the
+    # plan's range (0.25 h .. h, never above the plan's FP64 h), one factor for both
+    # axes, deterministic, and narrower where points are dense
+    w = synth.make_config(name)
+    bw = synth.adaptive_bandwidths(w)
+    assert bw.dtype == np.float32 and bw.shape == (w.n, 2) and bw.flags.c_contiguous
+    hs, ht = bw[:, 0].astype(np.float64), bw[:, 1].astype(np.float64)
+    assert (hs <= w.hs).all() and (ht <= w.ht).all()
+    assert (hs >= 0.25 * w.hs * (1 - 1e-6)).all() and (ht >= 0.25 * w.ht * (1 - 1e-6)).all()
+    np.testing.assert_allclose(hs / w.hs, ht / w.ht, rtol=1e-6)
+    assert np.array_equal(bw, synth.adaptive_bandwidths(w))
+    assert hs.min() < hs.max()                      # the recipe actually adapts
+    # dense cells get the narrow kernels: mean lambda of the densest decile < sparsest decile
+    p = w.points.astype(np.float64)
+    cell = np.floor(p / np.array([w.hs, w.hs, w.ht])).astype(np.int64)
+    _, inv, cnt = np.unique(cell, axis=0, return_inverse=True, return_counts=True)
+    c = cnt[inv.reshape(-1)]
+    lo, hi = np.quantile(c, [0.1, 0.9])
+    assert hs[c >= hi].mean() < hs[c <= lo].mean()
+
+
+def test_sweep_fractions():
+    f = synth.SWEEP_FRACTIONS
+    assert f[0] == 1.0 and all(0 < a <= 1 for a in f) and list(f) == sorted(f, reverse=True)
