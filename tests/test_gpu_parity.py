@@ -254,3 +254,37 @@ def test_edge_cases(S, oracle_mod):
         with pytest.raises(S.StkdeError) as e:
             S.Plan(max_n=1, device=0, **bad_g)
         assert e.value.code == -1
+
+
+def test_tc_tma_store_edges(S, oracle_mod):
+    # tcgen05 engine, T-aligned output rows (Gt % 4 == 0 -> TMA tensor-store epilogue) on a
+    # grid ragged in x, y and in the last T tile: the hardware-clipped box edges must match
+    # the oracle; a 4-aligned slab (TMA path) and an unaligned one (fallback stores) must
+    # equal the full grid's layers bitwise
+    g = G(37, 29, 132, hs=5.0, ht=9.0)
+    pts = make_points(700, g, True, seed=31)
+    gpu, C, info = run_gpu(S, pts, **g)
+    assert info["engine"] == 2 and info["Bt"] == 128
+    ref = oracle_mod.stkde_pb(pts, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="tma-edges")
+    assert C == ref.contributions
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=len(pts), device=0, **g) as p:
+        t = torch.from_numpy(pts).to(dev)
+        full = p.compute(t).cpu().numpy()
+        for t0, t1 in ((4, 68), (3, 67), (64, 128), (32, 100), (96, 132), (128, 132), (0, 132)):
+            s = p.compute_slab(t, t0, t1).cpu().numpy()
+            assert np.array_equal(s, full[:, :, t0:t1]), (t0, t1)
+        p.check()
+
+
+def test_large_bandwidth_falls_back(S, oracle_mod):
+    # H_s > 120 exceeds the tcgen05 engine's int8 chord table: the plan falls back to the
+    # mma.sync engine, same parity contract
+    g = G(270, 260, 12, hs=125.0, ht=3.0)
+    pts = make_points(25, g, False, seed=33)
+    gpu, C, info = run_gpu(S, pts, **g)
+    assert info["engine"] == 1
+    ref = oracle_mod.stkde_pb(pts, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="hs>120")
+    assert C == ref.contributions
