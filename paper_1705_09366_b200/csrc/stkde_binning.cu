@@ -120,53 +120,54 @@ __global__ void k_permute(const PointRec *__restrict__ rec, const uint32_t *__re
 // (1, 0) for an empty row; computed once per point instead of once per
 // (point, tile) visit.  Requires H_s <= 120.  Adaptive calls (bw != NULL): the
 // disc of point i has its own radius hs_i (the table layout keeps the plan's H_s).
+// One thread per (point, aligned 8-row block): the record is read once for 8 independent
+// rows and the block is one 16-byte store.
+__device__ __forceinline__ uint32_t chord_entry(const GridParams &g, const PointRec &r, int Y) {
+    int dl = 1, dh = 0;
+    if (Y >= r.Y - g.Hs && Y <= r.Y + g.Hs) {
+        // FP32 fast path in voxel-local coordinates: column X_i + k is inside iff
+        // (k - pc)^2 + dy^2 < r^2 with pc = fx - 0.5; it is exact unless a decision
+        // falls within the FP64 band (then row_chord re-decides with Alg. 1's FP64 gate)
+        const float dyv = (float)(Y - r.Y) + 0.5f - r.fy;
+        const float dy2 = __fmul_rn(dyv, dyv);
+        const float lo_b = g.rs2 * (1.0f - GATE_BAND), hi_b = g.rs2 * (1.0f + GATE_BAND);
+        bool exact = false;
+        if (dy2 > hi_b) {
+            exact = true;                                  // empty row
+        } else if (dy2 < lo_b) {
+            const float pc = r.fx - 0.5f;
+            const float c = sqrtf(g.rs2 - dy2);
+            const int a = (int)floorf(pc - c) + 1, b = (int)ceilf(pc + c) - 1;
+            auto d2 = [&](int k) { const float dx = (float)k - pc; return __fadd_rn(__fmul_rn(dx, dx), dy2); };
+            if (a <= b && d2(a) < lo_b && d2(b) < lo_b && d2(a - 1) > hi_b && d2(b + 1) > hi_b) {
+                dl = a; dh = b;
+                exact = true;
+            }
+        }
+        if (!exact) {
+            int lo, hi;
+            row_chord(g, r, Y, &lo, &hi);
+            if (lo <= hi) { dl = lo - r.X; dh = hi - r.X; }
+        }
+    }
+    return (uint32_t)((uint8_t)(int8_t)dl) | ((uint32_t)(uint8_t)(int8_t)dh << 8);
+}
+
 __global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams gp, uint16_t *__restrict__ chords,
                          const PointBw *__restrict__ bw) {
-    const int rows = chord_rows(gp.Hs);
-    const int64_t total = n * rows;
-    const bool small = total < ((int64_t)1 << 31);   // 32-bit index division (the 64-bit one is ~4x dearer)
+    const int nb = chord_rows(gp.Hs) / 8;            // 8-row blocks per point
+    const int64_t total = n * nb;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        int64_t i;
-        int j;
-        if (small) {
-            const uint32_t e32 = (uint32_t)e, i32 = e32 / (uint32_t)rows;
-            i = i32;
-            j = (int)(e32 - i32 * (uint32_t)rows);
-        } else {
-            i = e / rows;
-            j = (int)(e - i * rows);
-        }
+        const int64_t i = e / nb;
+        const int blk = (int)(e - i * nb);
         const PointRec r = rec[i];
         const GridParams g = bw ? with_point_bw(gp, bw[i]) : gp;
-        const int Y = ((r.Y - g.Hs) & ~7) + j;
-        int dl = 1, dh = 0;
-        if (Y >= r.Y - g.Hs && Y <= r.Y + g.Hs) {
-            // FP32 fast path in voxel-local coordinates: column X_i + k is inside iff
-            // (k - pc)^2 + dy^2 < r^2 with pc = fx - 0.5; it is exact unless a decision
-            // falls within the FP64 band (then row_chord re-decides with Alg. 1's FP64 gate)
-            const float dyv = (float)(Y - r.Y) + 0.5f - r.fy;
-            const float dy2 = __fmul_rn(dyv, dyv);
-            const float lo_b = g.rs2 * (1.0f - GATE_BAND), hi_b = g.rs2 * (1.0f + GATE_BAND);
-            bool exact = false;
-            if (dy2 > hi_b) {
-                exact = true;                                  // empty row
-            } else if (dy2 < lo_b) {
-                const float pc = r.fx - 0.5f;
-                const float c = sqrtf(g.rs2 - dy2);
-                const int a = (int)floorf(pc - c) + 1, b = (int)ceilf(pc + c) - 1;
-                auto d2 = [&](int k) { const float dx = (float)k - pc; return __fadd_rn(__fmul_rn(dx, dx), dy2); };
-                if (a <= b && d2(a) < lo_b && d2(b) < lo_b && d2(a - 1) > hi_b && d2(b + 1) > hi_b) {
-                    dl = a; dh = b;
-                    exact = true;
-                }
-            }
-            if (!exact) {
-                int lo, hi;
-                row_chord(g, r, Y, &lo, &hi);
-                if (lo <= hi) { dl = lo - r.X; dh = hi - r.X; }
-            }
-        }
-        chords[e] = (uint16_t)((uint8_t)(int8_t)dl | ((uint16_t)(uint8_t)(int8_t)dh << 8));
+        const int Y0 = ((r.Y - g.Hs) & ~7) + 8 * blk;
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w[k] = chord_entry(g, r, Y0 + 2 * k) | (chord_entry(g, r, Y0 + 2 * k + 1) << 16);
+        reinterpret_cast<uint4 *>(chords)[e] = make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -313,9 +314,9 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
 }
 
 int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
-    const int64_t total = n * chord_rows(p->g.Hs);
+    const int64_t total = n * (chord_rows(p->g.Hs) / 8);
     if (total > 0) {
-        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 16);
+        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 32);
         k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr);
         p->last_own_launches += 1;
     }
