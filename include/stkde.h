@@ -109,10 +109,12 @@ int stkde_compute_slab(stkde_plan_t plan, const float *d_points, int64_t n,
                        int64_t n_norm, int64_t t_begin, int64_t t_end,
                        float *d_slab, void *stream);
 
-/* Cost-balanced, Bt-aligned time-slab cuts for `nparts` devices.
+/* Cost-balanced, Bt-aligned time-slab cuts for `nparts` devices (tcgen05
+ * engine: when nparts exceeds ceil(Gt/Bt) the cut granularity is halved down
+ * to 32 layers -- its slabs are bitwise equal to the full grid at any boundary).
  * Synchronous (reads a per-layer cost histogram back to the host).  Writes
  * h_cuts[0..nparts] with h_cuts[0] = 0 and h_cuts[nparts] = Gt; empty
- * slabs are never produced while nparts <= ceil(Gt/Bt).  Cost per layer
+ * slabs are never produced while nparts <= ceil(Gt/granularity).  Cost per layer
  * T = alpha * (Gx*Gy*4 B)/B_hbm + beta * 2*W(T)/P_fp32 where W(T) is the
  * number of (point, column) pairs whose window contains T. */
 int stkde_slab_partition(stkde_plan_t plan, const float *d_points, int64_t n,
@@ -168,6 +170,25 @@ int stkde_count_contributions_adaptive(stkde_plan_t plan, const float *d_points,
  * tolerance.  Errors: STKDE_EINVAL (bad bandwidth / NULL grid), STKDE_ECAPACITY. */
 int stkde_compute_sweep(stkde_plan_t plan, const float *d_points, int64_t n, int nbw, const double *h_hs,
                         const double *h_ht, float *const *d_grids, void *stream);
+
+/* ---- X-slabs: the multi-GPU partition along X ----
+ * stkde_compute_xslab computes grid rows [x_begin, x_end) -- a contiguous block of
+ * the [Gx][Gy][Gt] layout -- into d_xslab (float32 [x_end - x_begin][Gy][Gt],
+ * fully overwritten), normalised with n_norm (the global n).  x_begin and x_end
+ * (unless = Gx) must be multiples of 16 (the tile width): the slab's tiles and their
+ * candidate lists are then the full grid's, so the result is bitwise equal to those
+ * rows of stkde_compute and the work splits without overhead.  tcgen05 engine only
+ * (else STKDE_EINVAL).  Asynchronous. */
+int stkde_compute_xslab(stkde_plan_t plan, const float *d_points, int64_t n, int64_t n_norm,
+                        int64_t x_begin, int64_t x_end, float *d_xslab, void *stream);
+/* Cost-balanced x cuts (multiples of 16, h_cuts[0] = 0, h_cuts[nparts] = Gx); the cost of
+ * column X is Gy*Gt*4 B / B_hbm + 2 W(X) / P_fp32, W(X) = sum_i 2 sqrt(rs^2 - (X - X_i)^2)
+ * (2 rt + 1).  stkde_xslab_partition reads the X_i histogram from the device
+ * (synchronous); stkde_xslab_cuts is its host-only half (rs = hs/sres, rt = ht/tres). */
+int stkde_xslab_partition(stkde_plan_t plan, const float *d_points, int64_t n, int nparts, int64_t *h_cuts,
+                          void *stream);
+int stkde_xslab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, double rs, double rt, const int64_t *h_hist_X, int nparts,
+                     int64_t *h_cuts);
 
 /* Single-process multi-device driver: plans[d] lives on device d's ordinal,
  * d_points[d] holds the full point set on that device, d_slabs[d] receives

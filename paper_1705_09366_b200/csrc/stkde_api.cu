@@ -125,6 +125,8 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     g.Ra = (g.Hs + BX - 1) / BX;
     g.Ray = (g.Hs + BYv - 1) / BYv;
     g.Rt = (g.Ht + BT - 1) / BT;
+    g.XA0 = 0;
+    g.NXA = g.NTX;
     // Home-bucket depth in T: the tcgen05 engine bins points into 16x8x32 (16 when
     // H_t <= 8) blocks so a tile fetches only the blocks its temporal reach meets;
     // the legacy engines bin by whole tiles.
@@ -144,7 +146,8 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     // Work-item and split-slot bounds: total candidates <= n * buckets per tile.
     const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ray + 1, g.NTY) * ncc_max;
     const int64_t cand_bound = std::max<int64_t>(max_n, 1) * nb;
-    const size_t tile_bytes = (size_t)(p->engine == STKDE_ENGINE_TC ? 128 : 256) * BT * 4;
+    // split-tile partial slot: tcgen05 engine int64 exact sums per voxel, legacy engines FP32
+    const size_t tile_bytes = (size_t)(p->engine == STKDE_ENGINE_TC ? 128 * 8 : 256 * 4) * BT;
     const int64_t slot_budget = (int64_t)env_int("STKDE_SLOT_MB", 1024) * (1 << 20) / (int64_t)tile_bytes;
     int64_t chunk = std::max<int64_t>(env_int("STKDE_CHUNK", 4096), (2 * cand_bound + slot_budget - 1) / slot_budget);
     // tcgen05 engine: the S32 accumulators take <= 129888 per point (D16: hl + mm + lh
@@ -203,6 +206,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
         {(void **)&p->partials, (size_t)p->max_slots * tile_bytes},
         {(void **)&p->counters, 128 * 4},
         {(void **)&p->hist_t, ((size_t)Gt + 1) * 4},
+        {(void **)&p->hist_x, ((size_t)Gx + 1) * 4},
         {(void **)&p->cub_tmp, p->cub_bytes},
     };
     size_t total = 0;
@@ -286,7 +290,11 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
     const double kc = p->kernel == STKDE_KERNEL_PRINTED ? M_PI / 2.0 : 2.0 / M_PI;
     const float cnorm = d_bw ? (float)(kc / ((double)n_norm * (g.sres * g.sres) * g.tres))
                              : (float)(kc / ((double)n_norm * (g.hs * g.hs) * g.ht));
-    int rc = launch_binning(p, d_points, n, st);
+    // the tcgen05 engine bins only the points that reach the slab (its integer sums do not
+    // depend on the candidate grouping); the FP32 engines keep the full binning so a slab
+    // stays bitwise equal to the full grid's layers
+    const bool slab_cull = p->engine == STKDE_ENGINE_TC;
+    int rc = launch_binning(p, d_points, n, st, slab_cull ? t_begin : 0, slab_cull ? t_end : (int64_t)g.Gt);
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     if (p->engine == STKDE_ENGINE_TC) {
         rc = launch_chords(p, n, st);
@@ -396,7 +404,7 @@ extern "C" int stkde_compute_sweep(stkde_plan_t p, const float *d_points, int64_
         for (int k = 0; k < nbw; ++k) CK(cudaMemsetAsync(d_grids[k], 0, vox * sizeof(float), st));
         return STKDE_OK;
     }
-    int rc = launch_binning(p, d_points, n, st);           // once, at the plan's (largest) reach
+    int rc = launch_binning(p, d_points, n, st, 0, g0.Gt);   // once, at the plan's (largest) reach
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     const double kc = p->kernel == STKDE_KERNEL_PRINTED ? M_PI / 2.0 : 2.0 / M_PI;
     const int c0 = 0, c1 = g0.NTT;
@@ -459,6 +467,95 @@ extern "C" int stkde_slab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, int Bt, int H
     return STKDE_OK;
 }
 
+// ---- x-slabs (multi-GPU partition along X) ----
+// Per-column cost: alpha * Gy*Gt*4 B / B_hbm + beta * 2 W(X) / P_fp32 with W(X) = sum_i
+// chord_i(X) * (2 rt + 1), chord_i(X) = 2 sqrt(rs^2 - (X - X_i)^2) (the disc's extent in Y
+// at column X times the window's layers); cuts at multiples of 16 columns (tile width).
+extern "C" int stkde_xslab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, double rs, double rt, const int64_t *h_hist_X,
+                                int nparts, int64_t *h_cuts) {
+    if (!h_cuts || !h_hist_X || nparts < 1 || Gx < 1 || Gy < 1 || Gt < 1 || !(rs > 0) || !(rt > 0)) {
+        set_error("bad arguments to stkde_xslab_cuts");
+        return STKDE_EINVAL;
+    }
+    const double B_hbm = 6.5e12, P_fp32 = 6.0e13;
+    const int R = (int)std::ceil(rs);
+    std::vector<double> chord(2 * R + 1);
+    for (int d = -R; d <= R; ++d) chord[d + R] = 2.0 * std::sqrt(std::max(rs * rs - (double)d * d, 0.0));
+    const int64_t nblk = (Gx + BX - 1) / BX;
+    std::vector<double> cost(nblk, 0.0);
+    for (int64_t X = 0; X < Gx; ++X) {
+        double w = 0.0;
+        for (int d = -R; d <= R; ++d) {
+            const int64_t Xi = X - d;
+            if (Xi >= 0 && Xi < Gx) w += (double)h_hist_X[Xi] * chord[d + R];
+        }
+        cost[X / BX] += (double)Gy * Gt * 4.0 / B_hbm + 2.0 * w * (2.0 * rt + 1.0) / P_fp32;
+    }
+    std::vector<double> cum(nblk + 1, 0.0);
+    for (int64_t b = 0; b < nblk; ++b) cum[b + 1] = cum[b] + cost[b];
+    const double tot = cum[nblk];
+    h_cuts[0] = 0;
+    int64_t prev = 0;
+    for (int k = 1; k < nparts; ++k) {
+        const double target = tot * k / nparts;
+        int64_t b = prev + 1;
+        while (b < nblk && cum[b] < target) ++b;
+        if (b > prev + 1 && (target - cum[b - 1]) < (cum[b] - target)) --b;
+        b = std::min<int64_t>(b, nblk - (nparts - k));
+        b = std::max<int64_t>(b, std::min<int64_t>(prev + 1, nblk));
+        h_cuts[k] = std::min<int64_t>(b * BX, Gx);
+        prev = b;
+    }
+    h_cuts[nparts] = Gx;
+    for (int k = 1; k <= nparts; ++k)
+        if (h_cuts[k] < h_cuts[k - 1]) h_cuts[k] = h_cuts[k - 1];
+    return STKDE_OK;
+}
+
+extern "C" int stkde_xslab_partition(stkde_plan_t p, const float *d_points, int64_t n, int nparts, int64_t *h_cuts,
+                                     void *stream) {
+    if (!p || !h_cuts || nparts < 1) { set_error("bad arguments"); return STKDE_EINVAL; }
+    const GridParams &g = p->g;
+    CK(cudaSetDevice(p->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    std::vector<int> hist(g.Gx + 1, 0);
+    if (n > 0) {
+        int rc = launch_hist_x(p, d_points, n, st);
+        if (rc) { set_error("histogram launch failed"); return rc; }
+        CK(cudaMemcpyAsync(hist.data(), p->hist_x, g.Gx * sizeof(int), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    std::vector<int64_t> h64(hist.begin(), hist.begin() + g.Gx);
+    return stkde_xslab_cuts(g.Gx, g.Gy, g.Gt, (double)g.rs, (double)g.rt, h64.data(), nparts, h_cuts);
+}
+
+extern "C" int stkde_compute_xslab(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm,
+                                   int64_t x_begin, int64_t x_end, float *d_xslab, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    const GridParams g0 = p->g;
+    if (p->engine != STKDE_ENGINE_TC) { set_error("x-slabs need the tcgen05 engine"); return STKDE_EINVAL; }
+    if (x_begin < 0 || x_end > g0.Gx || x_begin >= x_end || x_begin % BX != 0 || (x_end % BX != 0 && x_end != g0.Gx)) {
+        set_error("x-slab [x_begin, x_end) must satisfy 0 <= x_begin < x_end <= Gx with x_begin and x_end "
+                  "(unless = Gx) multiples of 16");
+        return STKDE_EINVAL;
+    }
+    if (!d_xslab) { set_error("NULL device pointer"); return STKDE_EINVAL; }
+    if (n < 0 || n_norm < 0) { set_error("n must be >= 0"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    if (n == 0 || n_norm == 0) {
+        p->last_own_launches = p->last_cub_calls = 0;
+        CK(cudaMemsetAsync(d_xslab, 0, (size_t)(x_end - x_begin) * g0.Gy * g0.Gt * sizeof(float), (cudaStream_t)stream));
+        return STKDE_OK;
+    }
+    p->g.XA0 = (int)(x_begin / BX);
+    p->g.NXA = (int)((x_end + BX - 1) / BX - x_begin / BX);
+    // the tile kernel indexes the full grid; the slab is that grid's block of rows [x_begin, x_end)
+    float *out_shifted = d_xslab - x_begin * (int64_t)g0.Gy * g0.Gt;
+    const int rc = compute_slab_impl(p, d_points, n, n_norm, 0, g0.Gt, out_shifted, (cudaStream_t)stream);
+    p->g = g0;
+    return rc;
+}
+
 extern "C" int stkde_slab_partition(stkde_plan_t p, const float *d_points, int64_t n, int nparts, int64_t *h_cuts,
                                     void *stream) {
     if (!p || !h_cuts || nparts < 1) { set_error("bad arguments"); return STKDE_EINVAL; }
@@ -473,7 +570,13 @@ extern "C" int stkde_slab_partition(stkde_plan_t p, const float *d_points, int64
         CK(cudaStreamSynchronize(st));
     }
     std::vector<int64_t> h64(hist.begin(), hist.begin() + g.Gt);
-    return stkde_slab_cuts(g.Gx, g.Gy, g.Gt, g.BT, g.Ht, (double)g.rs, h64.data(), nparts, h_cuts);
+    // cut granularity: Bt; the tcgen05 engine (slabs bitwise equal at any boundary, TMA
+    // epilogue for 32-aligned starts) halves it down to 32 layers while there are fewer
+    // Bt blocks than parts (stress at 8 ranks: 64-layer slabs instead of 4 busy ranks)
+    int gran = g.BT;
+    if (p->engine == STKDE_ENGINE_TC)
+        while (gran > 32 && (g.Gt + gran - 1) / gran < nparts) gran /= 2;
+    return stkde_slab_cuts(g.Gx, g.Gy, g.Gt, gran, g.Ht, (double)g.rs, h64.data(), nparts, h_cuts);
 }
 
 extern "C" int stkde_compute_sharded(stkde_plan_t *plans, int ndev, const float *const *d_points, int64_t n,

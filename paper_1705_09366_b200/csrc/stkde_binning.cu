@@ -67,7 +67,8 @@ __device__ __forceinline__ bool make_bw(const GridParams &g, const float *__rest
 __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, PointRec *__restrict__ rec,
                        uint32_t *__restrict__ keys, uint32_t *__restrict__ vals,
                        uint32_t *__restrict__ bucket_cnt, int *__restrict__ err, uint32_t sentinel,
-                       const float *__restrict__ bw, PointBw *__restrict__ bw_rec, unsigned *__restrict__ wmax) {
+                       const float *__restrict__ bw, PointBw *__restrict__ bw_rec, unsigned *__restrict__ wmax,
+                       int t_begin, int t_end) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float x = pts[3 * i], y = pts[3 * i + 1], t = pts[3 * i + 2];
@@ -87,7 +88,9 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
     if (!make_rec(g, x, y, t, &r)) {
         atomicOr(err, 1);
         r = PointRec{0, 0, 0, 0.f, 0.f, 0.f, 0.f, 0.f};
-    } else if (bw_ok && reaches_grid(g, r)) {
+    } else if (bw_ok && reaches_grid(g, r) && r.T + g.Ht >= t_begin && r.T - g.Ht < t_end &&
+               r.X + g.Hs >= g.XA0 * BX && r.X - g.Hs < (g.XA0 + g.NXA) * BX) {
+        // (points whose window [T_i - H_t, T_i + H_t] misses the requested slab are not binned)
         int a = min(max(r.X, 0), g.Gx - 1) / BX;
         int b = min(max(r.Y, 0), g.Gy - 1) / g.BY;
         int c = min(max(r.T, 0), g.Gt - 1) / g.BTH;
@@ -103,9 +106,9 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
 // in the tile kernel).
 __global__ void k_permute(const PointRec *__restrict__ rec, const uint32_t *__restrict__ vals,
                           PointRec *__restrict__ out, int64_t n, const PointBw *__restrict__ bw_rec,
-                          PointBw *__restrict__ bw_out) {
+                          PointBw *__restrict__ bw_out, const uint32_t *__restrict__ nbinned) {
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < n) {
+    if (j < n && j < (int64_t)*nbinned) {      // the unbinned (sentinel-key) records sort last
         const uint32_t v = vals[j];
         out[j] = rec[v];
         if (bw_rec) bw_out[j] = bw_rec[v];
@@ -154,9 +157,9 @@ __device__ __forceinline__ uint32_t chord_entry(const GridParams &g, const Point
 }
 
 __global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams gp, uint16_t *__restrict__ chords,
-                         const PointBw *__restrict__ bw) {
+                         const PointBw *__restrict__ bw, const uint32_t *__restrict__ nbinned) {
     const int nb = chord_rows(gp.Hs) / 8;            // 8-row blocks per point
-    const int64_t total = n * nb;
+    const int64_t total = min(n, (int64_t)*nbinned) * nb;   // binned points only (they sort first)
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / nb;
         const int blk = (int)(e - i * nb);
@@ -192,7 +195,7 @@ __global__ void k_tile_counts(GridParams g, const uint32_t *__restrict__ bucket_
                               uint32_t *__restrict__ lkey, uint32_t *__restrict__ lval) {
     int ls = blockIdx.x * blockDim.x + threadIdx.x;
     if (ls >= nsl) return;
-    int a = ls % g.NTX, b = (ls / g.NTX) % g.NTY, c = ls / (g.NTX * g.NTY) + c0;
+    int a = ls % g.NXA + g.XA0, b = (ls / g.NXA) % g.NTY, c = ls / (g.NXA * g.NTY) + c0;
     uint32_t cnt = tile_candidates(g, bucket_begin, a, b, c);
     lkey[ls] = 0xFFFFFFFFu - cnt;
     lval[ls] = (uint32_t)ls;
@@ -275,6 +278,15 @@ __global__ void k_hist_t(const float *__restrict__ pts, int64_t n, GridParams g,
     atomicAdd(&hist[min(max(r.T, 0), g.Gt - 1)], 1);
 }
 
+// Histogram of X_i (clamped) for the x-slab partition.
+__global__ void k_hist_x(const float *__restrict__ pts, int64_t n, GridParams g, int *__restrict__ hist) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    PointRec r;
+    if (!make_rec(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], &r) || !reaches_grid(g, r)) return;
+    atomicAdd(&hist[min(max(r.X, 0), g.Gx - 1)], 1);
+}
+
 // Slab [t0,t1) of layout [Gx][Gy][t1-t0] -> full grid [Gx][Gy][Gt].
 // On the root of a multi-device run `slab` is a peer pointer (NVLink).
 __global__ void k_gather(const float *__restrict__ slab, int64_t rows, int64_t Gt, int64_t t0, int64_t ts,
@@ -290,24 +302,27 @@ __global__ void k_gather(const float *__restrict__ slab, int64_t rows, int64_t G
 // ----------------------------------------------------------- launchers ---
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
-int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st) {
+int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st, int64_t t_begin,
+                   int64_t t_end) {
     const GridParams &g = p->g;
     cudaMemsetAsync(p->bucket_cnt, 0, (p->nbuckets + 1) * sizeof(uint32_t), st);
     const bool ad = p->d_bw != nullptr;
     if (ad) cudaMemsetAsync(p->counters + 6, 0, sizeof(int), st);
     k_prep<<<nblk(n, 256), 256, 0, st>>>(d_points, n, g, p->rec, p->keys_in, p->vals_in, p->bucket_cnt,
                                           p->counters + 1, (uint32_t)p->nbuckets, p->d_bw,
-                                          ad ? p->bw_rec : nullptr, reinterpret_cast<unsigned *>(p->counters + 6));
+                                          ad ? p->bw_rec : nullptr, reinterpret_cast<unsigned *>(p->counters + 6),
+                                          (int)t_begin, (int)t_end);
     size_t bytes = p->cub_bytes;
     if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->keys_in, p->keys_out, p->vals_in, p->vals_out,
                                         (int)n, 0, p->key_bits, st) != cudaSuccess)
         return STKDE_ECUDA;
-    k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n, ad ? p->bw_rec : nullptr,
-                                             p->bw_sorted);
     bytes = p->cub_bytes;
     if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->bucket_cnt, p->bucket_begin, (int)(p->nbuckets + 1), st) !=
         cudaSuccess)
         return STKDE_ECUDA;
+    // bucket_begin[nbuckets] = the number of binned points (the sentinel bucket sorts last)
+    k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n, ad ? p->bw_rec : nullptr,
+                                             p->bw_sorted, p->bucket_begin + p->nbuckets);
     p->last_own_launches += 2;
     p->last_cub_calls += 2;
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
@@ -317,7 +332,8 @@ int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
     const int64_t total = n * (chord_rows(p->g.Hs) / 8);
     if (total > 0) {
         const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 32);
-        k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr);
+        k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr,
+                                         p->bucket_begin + p->nbuckets);
         p->last_own_launches += 1;
     }
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
@@ -325,7 +341,7 @@ int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
 
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
     const GridParams &g = p->g;
-    int nsl = g.NTX * g.NTY * (c1 - c0);
+    int nsl = g.NXA * g.NTY * (c1 - c0);
     k_tile_counts<<<nblk(nsl, 256), 256, 0, st>>>(g, p->bucket_begin, c0, nsl, p->lpt_key_in, p->lpt_val_in);
     size_t bytes = p->cub_bytes;
     if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->lpt_key_in, p->lpt_key_out, p->lpt_val_in,
@@ -354,6 +370,12 @@ int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_be
 int launch_hist_t(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st) {
     cudaMemsetAsync(p->hist_t, 0, (p->g.Gt + 1) * sizeof(int), st);
     if (n > 0) k_hist_t<<<nblk(n, 256), 256, 0, st>>>(d_points, n, p->g, p->hist_t);
+    return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
+}
+
+int launch_hist_x(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st) {
+    cudaMemsetAsync(p->hist_x, 0, (p->g.Gx + 1) * sizeof(int), st);
+    if (n > 0) k_hist_x<<<nblk(n, 256), 256, 0, st>>>(d_points, n, p->g, p->hist_x);
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }
 

@@ -59,6 +59,8 @@ struct GridParams {
     int BY, BT;             // tile width in Y (columns), tile height (layers)
     int BTH, NTTH;          // home-bucket depth in T (layers; BT for the legacy engines) and count
     int Ra, Ray, Rt;        // home-bucket reach in tiles: ceil(Hs/BX), ceil(Hs/BY), ceil(Ht/BT)
+    int XA0, NXA;           // x-tile window of the current launch: tiles [XA0, XA0 + NXA) (x-slabs;
+                            // the whole grid otherwise)
     int kernel;             // STKDE_KERNEL_*
 };
 
@@ -211,6 +213,7 @@ struct stkde_plan_s {
     int no_tma;                 // STKDE_NO_TMA: epilogue stores by per-column bulk copies instead of TMA
     void *debug_progress;       // stkde_plan_debug_progress: per-(CTA, warp) protocol state (host-mapped)
     int *hist_t;                // [Gt + 1] slab-partition histogram
+    int *hist_x;                // [Gx + 1] x-slab-partition histogram
     void *cub_tmp;
     size_t cub_bytes;
 
@@ -225,7 +228,9 @@ struct stkde_plan_s {
 
 namespace stkde {
 // launchers (stkde_binning.cu / stkde_tile.cu)
-int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
+// bins the points whose window reaches layers [t_begin, t_end) (the slab being computed)
+int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st, int64_t t_begin,
+                   int64_t t_end);
 int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st);
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,
@@ -233,6 +238,7 @@ int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end,
 int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_begin,
                  int64_t t_end, int64_t *d_count, cudaStream_t st, const float *d_bw = nullptr);
 int launch_hist_t(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
+int launch_hist_x(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
 int launch_gather(const float *slab, int64_t Gx, int64_t Gy, int64_t Gt, int64_t t0, int64_t t1,
                   float *full, cudaStream_t st);
 size_t tile_smem_bytes(int BT, int CT);

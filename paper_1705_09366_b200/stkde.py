@@ -26,7 +26,8 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
            "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress", "stkde_strerror",
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
-           "stkde_count_contributions_adaptive", "stkde_compute_sweep")
+           "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
+           "stkde_xslab_partition", "stkde_xslab_cuts")
 
 
 class StkdeError(RuntimeError):
@@ -79,6 +80,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_compute_adaptive_slab.argtypes = [P, P, P, I64, I64, I64, I64, P, P]
     L.stkde_count_contributions_adaptive.argtypes = [P, P, P, I64, I64, I64, P, P]
     L.stkde_compute_sweep.argtypes = [P, P, I64, I32, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(P), P]
+    L.stkde_compute_xslab.argtypes = [P, P, I64, I64, I64, I64, P, P]
+    L.stkde_xslab_partition.argtypes = [P, P, I64, I32, ctypes.POINTER(I64), P]
+    L.stkde_xslab_cuts.argtypes = [I64, I64, I64, D, D, ctypes.POINTER(I64), I32, ctypes.POINTER(I64)]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
@@ -88,7 +92,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
                  "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress",
                  "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
-                 "stkde_compute_sweep"):
+                 "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -229,6 +233,29 @@ class Plan:
             int(self.G[2] if t_end is None else t_end), out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
 
+    # -- x-slabs (include/stkde.h) --
+    def compute_xslab(self, points: torch.Tensor, x_begin: int, x_end: int, n_norm: Optional[int] = None,
+                      out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Grid rows [x_begin, x_end): [x_end - x_begin, Gy, Gt] float32 (bitwise those rows of compute)."""
+        pts = _points_arg(points, self.device)
+        shape = (int(x_end) - int(x_begin), self.G[1], self.G[2])
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=self.device)
+        if out.device != self.device or out.dtype != torch.float32 or not out.is_contiguous() or tuple(out.shape) != shape:
+            raise ValueError("out must be a contiguous float32 CUDA tensor of shape %s" % (shape,))
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        _check(load_library().stkde_compute_xslab(self._h, pts.data_ptr(), pts.shape[0], nn, int(x_begin), int(x_end),
+                                                  out.data_ptr(), _stream_ptr(stream, self.device)))
+        return out
+
+    def xslab_partition(self, points: torch.Tensor, nparts: int,
+                        stream: Optional[torch.cuda.Stream] = None) -> list:
+        pts = _points_arg(points, self.device)
+        cuts = (ctypes.c_int64 * (nparts + 1))()
+        _check(load_library().stkde_xslab_partition(self._h, pts.data_ptr(), pts.shape[0], int(nparts), cuts,
+                                                    _stream_ptr(stream, self.device)))
+        return [int(c) for c in cuts]
+
     # -- multi-bandwidth sweep (include/stkde.h) --
     def compute_sweep(self, points: torch.Tensor, hs: Sequence[float], ht: Sequence[float],
                       outs: Optional[Sequence[torch.Tensor]] = None,
@@ -345,3 +372,12 @@ def stkde(points: torch.Tensor, *, x0, y0, t0, sres, tres, Gx, Gy, Gt, hs, ht,
         out = p.compute(points)
         torch.cuda.current_stream(points.device).synchronize()
         return out
+
+
+def xslab_cuts(G, rs: float, rt: float, hist_X, nparts: int) -> list:
+    """Host-only cost-balanced x cuts (stkde_xslab_cuts): multiples of 16, [0 .. Gx]."""
+    L = load_library()
+    h = (ctypes.c_int64 * len(hist_X))(*[int(v) for v in hist_X])
+    cuts = (ctypes.c_int64 * (nparts + 1))()
+    _check(L.stkde_xslab_cuts(int(G[0]), int(G[1]), int(G[2]), float(rs), float(rt), h, int(nparts), cuts))
+    return [int(c) for c in cuts]

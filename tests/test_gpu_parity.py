@@ -288,3 +288,57 @@ def test_large_bandwidth_falls_back(S, oracle_mod):
     ref = oracle_mod.stkde_pb(pts, **g)
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="hs>120")
     assert C == ref.contributions
+
+
+def test_partition_finer_than_bt(S):
+    # more parts than Bt blocks (tcgen05 engine): the cost-balanced cuts refine to 32-layer
+    # multiples, no slab is empty, and every slab equals the full grid's layers bitwise
+    w = synth.make_config("dengue")            # Gt = 128 -> Bt = 64: 2 blocks
+    g = w.grid_kwargs()
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        assert p.info()["engine"] == 2
+        t = torch.from_numpy(w.points).to(dev)
+        full = p.compute(t).cpu().numpy()
+        cuts = p.slab_partition(t, 4)
+        assert cuts[0] == 0 and cuts[-1] == w.G[2]
+        assert all(b > a for a, b in zip(cuts[:-1], cuts[1:])), cuts
+        assert all(c % 32 == 0 for c in cuts[:-1]), cuts
+        for a, b in zip(cuts[:-1], cuts[1:]):
+            s = p.compute_slab(t, a, b, n_norm=w.n).cpu().numpy()
+            assert np.array_equal(s, full[:, :, a:b]), (a, b)
+        p.check()
+
+
+@pytest.mark.parametrize("name", ["dengue", "social"])
+def test_xslabs_equal_full_grid(S, name):
+    # x-slabs (multiples of 16 columns, tcgen05 engine) are the full grid's rows, bitwise;
+    # the cost-balanced x partition covers the grid with non-empty slabs
+    w = synth.make_config(name)
+    g = w.grid_kwargs()
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        t = torch.from_numpy(w.points).to(dev)
+        full = p.compute(t).cpu().numpy()
+        for n in (3, 8):
+            cuts = p.xslab_partition(t, n)
+            assert cuts[0] == 0 and cuts[-1] == w.G[0] and all(b > a for a, b in zip(cuts[:-1], cuts[1:]))
+            for a, b in zip(cuts[:-1], cuts[1:]):
+                s = p.compute_xslab(t, a, b, n_norm=w.n).cpu().numpy()
+                assert np.array_equal(s, full[a:b]), (a, b)
+        p.check()
+
+
+def test_xslab_ragged_grid(S):
+    # ragged x / y / unaligned G_t: the last x-slab ends at G_x, slabs still equal the full grid
+    g = G(45, 33, 70, hs=5.5, ht=7.0)
+    pts = make_points(800, g, True, seed=41)
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=len(pts), device=0, **g) as p:
+        t = torch.from_numpy(pts).to(dev)
+        full = p.compute(t).cpu().numpy()
+        for a, b in ((0, 16), (16, 45), (32, 45), (0, 45)):
+            s = p.compute_xslab(t, a, b).cpu().numpy()
+            assert np.array_equal(s, full[a:b]), (a, b)
+        with pytest.raises(S.StkdeError):
+            p.compute_xslab(t, 8, 24)                  # not a multiple of 16

@@ -104,3 +104,20 @@ def test_gloo_world2_gather_assemble(S, oracle_mod):
     for p in ps:
         p.join(timeout=60)
     assert res == {0: "ok", 1: "ok"}, res
+
+
+def test_xslab_cuts_host():
+    # stkde_xslab_cuts (host-only half of the x partition): multiples of 16, ordered, covering
+    # [0, Gx), no empty part while nparts <= Gx/16, and more cuts where the points are
+    import paper_1705_09366_b200 as S
+    Gx, Gy, Gt = 1024, 512, 256
+    uniform = [100] * Gx
+    for n in (1, 2, 4, 8):
+        c = S.xslab_cuts((Gx, Gy, Gt), 6.0, 4.0, uniform, n)
+        assert c[0] == 0 and c[-1] == Gx and len(c) == n + 1
+        assert all(b > a for a, b in zip(c[:-1], c[1:])) and all(x % 16 == 0 for x in c[:-1])
+        widths = [b - a for a, b in zip(c[:-1], c[1:])]
+        assert max(widths) - min(widths) <= 16          # uniform points: equal widths
+    skew = [10 ** 6 if x < 128 else 1 for x in range(Gx)]  # compute-dominated mass in the first 128 columns
+    c = S.xslab_cuts((Gx, Gy, Gt), 6.0, 4.0, skew, 4)
+    assert c[1] <= 128 and c[2] <= 128
