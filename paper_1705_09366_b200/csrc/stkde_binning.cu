@@ -96,7 +96,9 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
         int c = min(max(r.T, 0), g.Gt - 1) / g.BTH;
         key = (uint32_t)((c * g.NTY + b) * g.NTX + a);
     }
-    atomicAdd(&bucket_cnt[key], 1u);
+    // (unbinned points keep the sentinel key and sort last; they are not counted: with slab
+    // culling most points of a slab call are unbinned, and one shared counter serialised them)
+    if (key != sentinel) atomicAdd(&bucket_cnt[key], 1u);
     rec[i] = r;
     keys[i] = key;
     vals[i] = (uint32_t)i;
