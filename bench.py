@@ -230,10 +230,22 @@ def gpu_main(args, w, rank, world, local_rank):
     bw = torch.from_numpy(bw_host).to(dev) if bw_host is not None else None
     fr = synth.SWEEP_FRACTIONS
     sw_hs, sw_ht = [f * w.hs for f in fr], [f * w.ht for f in fr]
+    # N > 1: the fixed variant splits the grid into cost-balanced X-slabs (stkde_compute_xslab:
+    # the slab's tiles are the full grid's, so the work splits without overhead); the adaptive
+    # variant into cost-balanced time slabs (stkde_compute_adaptive_slab)
+    xsplit = world > 1 and variant == "fixed"
+    x0, x1 = 0, w.G[0]
     with torch.cuda.stream(stream):
-        cuts = plan.slab_partition(pts, world, stream=stream) if world > 1 else [0, w.G[2]]
-        t0, t1 = cuts[rank], cuts[rank + 1]
-        if t1 <= t0:
+        if xsplit:
+            xcuts = plan.xslab_partition(pts, world, stream=stream)
+            x0, x1 = xcuts[rank], xcuts[rank + 1]
+            cuts = [0, w.G[2]]
+        else:
+            cuts = plan.slab_partition(pts, world, stream=stream) if world > 1 else [0, w.G[2]]
+        t0, t1 = cuts[0 if xsplit else rank], cuts[1 if xsplit else rank + 1]
+        if xsplit:   # the metric's C is the whole grid's: count it on rank 0 only
+            C = int(plan.count_contributions(pts, 0, w.G[2], stream=stream).item()) if rank == 0 else 0
+        elif t1 <= t0:
             C = 0
         elif variant == "adaptive":
             C = int(plan.count_contributions_adaptive(pts, bw, t0, t1, stream=stream).item())
@@ -248,7 +260,8 @@ def gpu_main(args, w, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(Ct)
     C_total = int(Ct.item())
-    out = torch.empty((w.G[0], w.G[1], max(t1 - t0, 1)), dtype=torch.float32, device=dev)
+    out = (torch.empty((max(x1 - x0, 1), w.G[1], w.G[2]), dtype=torch.float32, device=dev) if xsplit else
+           torch.empty((w.G[0], w.G[1], max(t1 - t0, 1)), dtype=torch.float32, device=dev))
     outs = [out] + [torch.empty_like(out) for _ in fr[1:]] if variant == "sweep" else [out]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -259,6 +272,9 @@ def gpu_main(args, w, rank, world, local_rank):
             plan.compute_adaptive_slab(p_pts, p_bw, t0, t1, n_norm=w.n, out=out, stream=stream)
         elif variant == "sweep":
             plan.compute_sweep(p_pts, sw_hs, sw_ht, outs=outs, stream=stream)
+        elif xsplit:
+            if x1 > x0:
+                plan.compute_xslab(p_pts, x0, x1, n_norm=w.n, out=out, stream=stream)
         else:
             plan.compute_slab(p_pts, t0, t1, n_norm=w.n, out=out, stream=stream)
 
@@ -307,12 +323,23 @@ def gpu_main(args, w, rank, world, local_rank):
     # ---- e2e through the public API: pinned host points in, grid (slab) out ----
     host_pts = torch.from_numpy(w.points).pin_memory()
     host_bw = torch.from_numpy(bw_host).pin_memory() if bw_host is not None else None
-    host_outs = [torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory() for _ in outs]
+    host_outs = None
     e2e_steps = max(1, min(args.steps, 10))
     # fixed variant: the grid is produced as Bt-layer T-slabs (stkde_compute_slab) and slab k's
     # device->host copy runs on a second stream while slab k+1 is computed
     pipe = None
-    if variant == "fixed" and t1 > t0:
+    xpipe = None
+    if xsplit and x1 > x0:
+        # this rank's rows in 4 x sub-slabs (multiples of 16): sub-slab k's D2H into its rows of
+        # one pinned buffer overlaps sub-slab k+1's compute
+        step16 = max(16, ((x1 - x0) // 4 + 15) // 16 * 16)
+        xs = list(range(x0, x1, step16)) + [x1]
+        host_full = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory()
+        xpipe = [(a, b) for a, b in zip(xs[:-1], xs[1:])]
+        host_outs = [host_full]
+        copy_stream = torch.cuda.Stream(dev)
+        slab_ev = [torch.cuda.Event() for _ in xpipe]
+    elif variant == "fixed" and t1 > t0:
         Bt = info["Bt"]
         sc = list(range(t0, t1, Bt)) + [t1]
         pipe = [(a, b, torch.empty((w.G[0], w.G[1], b - a), dtype=torch.float32, device=dev),
@@ -321,6 +348,8 @@ def gpu_main(args, w, rank, world, local_rank):
         host_outs = [hb for _, _, _, hb in pipe]
         copy_stream = torch.cuda.Stream(dev)
         slab_ev = [torch.cuda.Event() for _ in pipe]
+    if host_outs is None:
+        host_outs = [torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory() for _ in outs]
     barrier()
     eb, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
@@ -328,7 +357,16 @@ def gpu_main(args, w, rank, world, local_rank):
         for _ in range(e2e_steps):
             dpts = host_pts.to(dev, non_blocking=True)
             dbw = host_bw.to(dev, non_blocking=True) if host_bw is not None else None
-            if pipe is None:
+            if xpipe is not None:
+                stream.wait_stream(copy_stream)
+                for (a, b), ev in zip(xpipe, slab_ev):
+                    plan.compute_xslab(dpts, a, b, n_norm=w.n, out=out[a - x0:b - x0], stream=stream)
+                    ev.record(stream)
+                    copy_stream.wait_event(ev)
+                    with torch.cuda.stream(copy_stream):
+                        host_full[a - x0:b - x0].copy_(out[a - x0:b - x0], non_blocking=True)
+                stream.wait_stream(copy_stream)
+            elif pipe is None:
                 run(dpts, dbw)
                 for ho, o in zip(host_outs, outs):
                     ho.copy_(o, non_blocking=True)
@@ -376,11 +414,12 @@ def gpu_main(args, w, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (the tile kernel) ----
     (hbm_peak, hbm_src), (bf16_peak, bf16_src) = peaks()
-    grid_bytes = w.G[0] * w.G[1] * (t1 - t0) * 4 * len(outs)
-    t_fp32 = 2.0 * C / (FP32_NOMINAL_TFLOPS * 1e12)
+    grid_bytes = (x1 - x0) * w.G[1] * (t1 - t0) * 4 * len(outs)
     t_hbm = grid_bytes / (hbm_peak * 1e9)
+    C_rank = C_total / world if xsplit else C       # x-slabs: per-rank work ~ C / N (cost-balanced cuts)
+    t_fp32 = 2.0 * C_rank / (FP32_NOMINAL_TFLOPS * 1e12)
     if t_fp32 >= t_hbm:
-        ach = 2.0 * C / (kernel_ms * 1e-3) / 1e12
+        ach = 2.0 * C_rank / (kernel_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": ach, "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP32_NOMINAL_TFLOPS,
                 "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1.965 GHz (DESIGN.md §4); "
@@ -392,7 +431,7 @@ def gpu_main(args, w, rank, world, local_rank):
     roof["traffic"] = profile_traffic(w.name, info["engine"], variant)
     roof["kernel"] = KERNELS[info["engine"]] % info["Bt"]
     roof["kernel_ms"] = kernel_ms_max
-    roof["algorithmic"] = {"flops": 2 * C, "bytes": grid_bytes,
+    roof["algorithmic"] = {"flops": 2 * C_rank, "bytes": grid_bytes,
                            "per_unit": "2 FLOP per contribution (one FMA acc += K_s*K_t), 4 B per voxel written once"}
     # the tensor pipe's own roofline (tcgen05 engine): int8 ops the kernel issued per launch
     # (7 MMAs of 128 x N x 32 per k-block, 2 ops per MAC) against the dense int8 peak
@@ -407,7 +446,7 @@ def gpu_main(args, w, rank, world, local_rank):
                    "mean_mma_n": mma_cols / mma_kblocks,
                    # contributions / (128 x N x 32 products per k-block): the share of the
                    # tile contraction that is inside some disc and window
-                   "useful_fraction": C / (128 * 32 * mma_cols / args.steps)}
+                   "useful_fraction": C_rank / (128 * 32 * mma_cols / args.steps)}
 
     result = None
     if rank == 0:
@@ -426,12 +465,15 @@ def gpu_main(args, w, rank, world, local_rank):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": config_dict(w, info, dict(variant_config(variant), **{
                 "contributions": C_total, "ms_per_grid": ms_max / len(outs),
-                "parallelism": "time-slab x%d" % world, "slab_cuts": cuts,
+                "parallelism": ("x-slab x%d" if xsplit else "time-slab x%d") % world,
+                "slab_cuts": xcuts if xsplit else cuts,
                 "l2": "flushed between timed steps (256 MiB write, untimed)",
                 "inputs_resident": True})),
             "e2e": {"value": C_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
-                    "pipeline": ("%d T-slabs of Bt layers; D2H of slab k overlaps the compute of slab k+1"
+                    "pipeline": ("%d x sub-slabs per rank; D2H of sub-slab k overlaps the compute of k+1"
+                                 % len(xpipe)) if xpipe else
+                                ("%d T-slabs of Bt layers; D2H of slab k overlaps the compute of slab k+1"
                                  % len(pipe)) if pipe else "compute, then D2H"},
             "gpu_launches": own * args.steps,
             "library_launches": {"cub_calls": cub * args.steps},
