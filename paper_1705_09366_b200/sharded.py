@@ -1,13 +1,15 @@
-"""Time-slab multi-GPU decomposition (one process per GPU, torch.distributed).
+"""Multi-GPU decomposition into slabs (one process per GPU, torch.distributed).
 
-The grid is cut along T into contiguous, cost-balanced slabs whose
-boundaries are multiples of the tile height Bt (stkde_slab_partition).  Every
-rank holds the full point set and computes only its slab with
-stkde_compute_slab; points whose temporal window misses the slab are culled on
-the device, so the halo of PAPER.md:415-433's temporal split is implicit and no
-reduction is needed: voxel tiles are independent.  There is NO collective on
-the data path.  Because slab boundaries are Bt-aligned, every rank's slab is
-bitwise equal to the same layers of a single-GPU run.
+The grid is cut into contiguous, cost-balanced slabs along X (axis "x":
+stkde_xslab_partition / stkde_compute_xslab, rows [x0, x1) at multiples of the
+16-column tile width -- the default for the tcgen05 engine, whose slab tiles are
+the full grid's) or along T (axis "t": stkde_slab_partition / stkde_compute_slab,
+the temporal split of PAPER.md:415-433; Bt-aligned cuts, refined to 32 layers by
+the tcgen05 engine).  Every rank holds the full point set and computes only its
+slab; points that cannot reach the slab are culled on the device, so the halo is
+implicit and no reduction is needed: voxel tiles are independent.  There is NO
+collective on the data path, and every rank's slab is bitwise equal to the same
+block of a single-GPU run.
 
 `gather_slabs` is the optional whole-grid gather to one rank (NCCL point-to-
 point over NVLink on GPUs, gloo on CPU in the tests); `assemble` writes the
@@ -27,53 +29,73 @@ def rank_slab(cuts: Sequence[int], rank: int):
     return int(cuts[rank]), int(cuts[rank + 1])
 
 
-def validate_cuts(cuts: Sequence[int], Gt: int, Bt: int) -> None:
-    """Cuts cover [0, Gt), are non-decreasing and Bt-aligned (except the last)."""
-    if cuts[0] != 0 or cuts[-1] != Gt:
-        raise ValueError("cuts must start at 0 and end at Gt: %s" % (list(cuts),))
+def validate_cuts(cuts: Sequence[int], extent: int, granule: int) -> None:
+    """Cuts cover [0, extent), are non-decreasing and multiples of `granule` (except the last)."""
+    if cuts[0] != 0 or cuts[-1] != extent:
+        raise ValueError("cuts must start at 0 and end at %d: %s" % (extent, list(cuts)))
     for a, b in zip(cuts[:-1], cuts[1:]):
         if b < a:
             raise ValueError("cuts must be non-decreasing: %s" % (list(cuts),))
     for c in cuts[1:-1]:
-        if c % Bt:
-            raise ValueError("interior cuts must be multiples of Bt=%d: %s" % (Bt, list(cuts)))
+        if c % granule:
+            raise ValueError("interior cuts must be multiples of %d: %s" % (granule, list(cuts)))
 
 
 class ShardedSTKDE:
     """Per-rank driver: plan on the local GPU, this rank's slab, optional gather."""
 
     def __init__(self, points: torch.Tensor, *, grid: dict, rank: int, world: int, kernel: int = 0,
-                 cuts: Optional[Sequence[int]] = None):
+                 cuts: Optional[Sequence[int]] = None, axis: Optional[str] = None):
         self.rank, self.world = rank, world
         self.points = points
         self.plan = Plan(max_n=max(int(points.shape[0]), 1), kernel=kernel, device=points.device.index, **grid)
         self.G = self.plan.G
-        self.Bt = self.plan.info()["Bt"]
+        info = self.plan.info()
+        self.Bt = info["Bt"]
+        tc = info["engine"] == 2
+        self.axis = axis if axis is not None else ("x" if tc else "t")
+        if self.axis not in ("x", "t"):
+            raise ValueError("axis must be 'x' or 't'")
         # Every rank derives the same cuts from the same points (no collective).
-        self.cuts = list(cuts) if cuts is not None else self.plan.slab_partition(points, world)
-        validate_cuts(self.cuts, self.G[2], self.Bt)
-        self.t0, self.t1 = rank_slab(self.cuts, rank)
+        if self.axis == "x":
+            self.cuts = list(cuts) if cuts is not None else self.plan.xslab_partition(points, world)
+            validate_cuts(self.cuts, self.G[0], 16)
+        else:
+            self.cuts = list(cuts) if cuts is not None else self.plan.slab_partition(points, world)
+            validate_cuts(self.cuts, self.G[2], 32 if tc else self.Bt)
+        self.s0, self.s1 = rank_slab(self.cuts, rank)
 
     def compute(self, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
-        """This rank's slab [Gx, Gy, t1-t0], normalised with the global n."""
+        """This rank's slab ([x1-x0, Gy, Gt] or [Gx, Gy, t1-t0]), normalised with the global n."""
+        n = int(self.points.shape[0])
+        if self.axis == "x":
+            if out is None:
+                out = torch.empty((self.s1 - self.s0, self.G[1], self.G[2]), dtype=torch.float32,
+                                  device=self.points.device)
+            if self.s1 > self.s0:
+                self.plan.compute_xslab(self.points, self.s0, self.s1, n_norm=n, out=out, stream=stream)
+            return out
         if out is None:
-            out = torch.empty((self.G[0], self.G[1], self.t1 - self.t0), dtype=torch.float32,
+            out = torch.empty((self.G[0], self.G[1], self.s1 - self.s0), dtype=torch.float32,
                               device=self.points.device)
-        if self.t1 > self.t0:
-            self.plan.compute_slab(self.points, self.t0, self.t1, n_norm=int(self.points.shape[0]), out=out,
-                                   stream=stream)
+        if self.s1 > self.s0:
+            self.plan.compute_slab(self.points, self.s0, self.s1, n_norm=n, out=out, stream=stream)
         return out
 
     def contributions(self) -> int:
-        if self.t1 <= self.t0:
+        """This rank's share of the metric's C (x axis: the whole count on rank 0, 0 elsewhere)."""
+        if self.axis == "x":
+            return int(self.plan.count_contributions(self.points).item()) if self.rank == 0 else 0
+        if self.s1 <= self.s0:
             return 0
-        return int(self.plan.count_contributions(self.points, self.t0, self.t1).item())
+        return int(self.plan.count_contributions(self.points, self.s0, self.s1).item())
 
     def close(self):
         self.plan.close()
 
 
-def gather_slabs(slab: torch.Tensor, cuts: Sequence[int], G, root: int = 0, group=None) -> Optional[List[torch.Tensor]]:
+def gather_slabs(slab: torch.Tensor, cuts: Sequence[int], G, root: int = 0, group=None,
+                 axis: str = "t") -> Optional[List[torch.Tensor]]:
     """Point-to-point gather of every rank's slab to `root` (returns the list on root)."""
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     if rank != root:
@@ -86,18 +108,22 @@ def gather_slabs(slab: torch.Tensor, cuts: Sequence[int], G, root: int = 0, grou
         if r == root:
             out.append(slab)
         else:
-            buf = torch.empty((G[0], G[1], t1 - t0), dtype=slab.dtype, device=slab.device)
+            shape = (t1 - t0, G[1], G[2]) if axis == "x" else (G[0], G[1], t1 - t0)
+            buf = torch.empty(shape, dtype=slab.dtype, device=slab.device)
             if buf.numel():
                 dist.recv(buf, src=r, group=group)
             out.append(buf)
     return out
 
 
-def assemble(slabs: Sequence[torch.Tensor], cuts: Sequence[int], G) -> torch.Tensor:
-    """Write per-rank slabs [Gx, Gy, t1-t0] into the full T-innermost grid [Gx, Gy, Gt]."""
+def assemble(slabs: Sequence[torch.Tensor], cuts: Sequence[int], G, axis: str = "t") -> torch.Tensor:
+    """Write per-rank slabs ([x1-x0, Gy, Gt] or [Gx, Gy, t1-t0]) into the full grid [Gx, Gy, Gt]."""
     full = torch.empty((G[0], G[1], G[2]), dtype=slabs[0].dtype, device=slabs[0].device)
     for r, s in enumerate(slabs):
-        t0, t1 = rank_slab(cuts, r)
-        if t1 > t0:
-            full[:, :, t0:t1] = s
+        a, b = rank_slab(cuts, r)
+        if b > a:
+            if axis == "x":
+                full[a:b] = s
+            else:
+                full[:, :, a:b] = s
     return full

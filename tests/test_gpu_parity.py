@@ -342,3 +342,22 @@ def test_xslab_ragged_grid(S):
             assert np.array_equal(s, full[a:b]), (a, b)
         with pytest.raises(S.StkdeError):
             p.compute_xslab(t, 8, 24)                  # not a multiple of 16
+
+
+@pytest.mark.parametrize("axis", ["x", "t"])
+def test_sharded_driver_axes(S, axis):
+    # the per-rank driver (sharded.ShardedSTKDE) for 3 ranks run in turn on one GPU: the
+    # assembled x- or time-slabs are the single-GPU grid, bitwise
+    from paper_1705_09366_b200.sharded import ShardedSTKDE, assemble
+    w = synth.make_config("dengue")
+    g = w.grid_kwargs()
+    t = torch.from_numpy(w.points).to(torch.device("cuda", 0))
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        full = p.compute(t).cpu()
+    slabs, cuts = [], None
+    for r in range(3):
+        d = ShardedSTKDE(t, grid=g, rank=r, world=3, axis=axis)
+        slabs.append(d.compute().cpu())
+        cuts = d.cuts
+        d.close()
+    assert torch.equal(assemble(slabs, cuts, w.G, axis=axis), full)

@@ -93,6 +93,49 @@ def _worker(rank, world, port, q):
         q.put((rank, repr(e)))
 
 
+def _worker_x(rank, world, port, q):
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        import oracle
+        import paper_1705_09366_b200 as S
+        from paper_1705_09366_b200.sharded import assemble, gather_slabs, rank_slab, validate_cuts
+        w = synth.make_config("dengue")
+        g = w.grid_kwargs()
+        hx = np.bincount(np.clip(np.floor(w.points[:, 0]).astype(np.int64), 0, w.G[0] - 1), minlength=w.G[0])
+        cuts = S.xslab_cuts(w.G, 8.0, 5.0, hx, world)
+        validate_cuts(cuts, w.G[0], 16)
+        allc = [None] * world
+        dist.all_gather_object(allc, cuts)
+        assert all(c == cuts for c in allc)
+        ref = oracle.stkde_pb(w.points, with_ambiguity=False, **g).vol
+        x0, x1 = rank_slab(cuts, rank)
+        slab = torch.from_numpy(np.ascontiguousarray(ref[x0:x1]))      # this rank's x-slab
+        got = gather_slabs(slab, cuts, w.G, root=0, axis="x")
+        if rank == 0:
+            full = assemble(got, cuts, w.G, axis="x").numpy()
+            assert np.array_equal(full, ref)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+
+
+def test_gloo_world2_xslab_gather_assemble(S, oracle_mod):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_x, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
+
+
 def test_gloo_world2_gather_assemble(S, oracle_mod):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
