@@ -143,8 +143,11 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     p->max_n = max_n;
     p->key_bits = key_bits_for(p->nbuckets);
 
-    // Work-item and split-slot bounds: total candidates <= n * buckets per tile.
-    const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ray + 1, g.NTY) * ncc_max;
+    // Work-item and split-slot bounds: total candidates <= n * (tiles a point is a candidate of):
+    // its home bucket (a, b, cc) lies in the reach of <= 2Ra+1 x-tiles, 2Ray+1 y-tiles and
+    // <= floor((BTH + 2 H_t + Bt - 2) / Bt) + 1 layer blocks (home_t_range)
+    const int64_t ntc = std::min<int64_t>((g.BTH + 2 * (int64_t)g.Ht + BT - 2) / BT + 1, g.NTT);
+    const int64_t nb = (int64_t)std::min(2 * g.Ra + 1, g.NTX) * std::min(2 * g.Ray + 1, g.NTY) * ntc;
     const int64_t cand_bound = std::max<int64_t>(max_n, 1) * nb;
     // split-tile partial slot: tcgen05 engine int64 exact sums per voxel, legacy engines FP32
     const size_t tile_bytes = (size_t)(p->engine == STKDE_ENGINE_TC ? 128 * 8 : 256 * 4) * BT;
