@@ -49,6 +49,12 @@ UNIT = "contributions/s"
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x 2 x max SM clock
 ENGINES = {0: "SIMT FP32 FFMA2", 1: "mma.sync m16n8k16 3xFP16", 2: "tcgen05.mma kind::i8, exact S32"}
 KERNELS = {0: "stkde::k_tile<Bt=%d>", 1: "stkde::k_tile_mma<Bt=%d>", 2: "stkde::k_tile_tc<Bt=%d>"}
+# the arithmetic type of the contraction (not a precision claim; NUMERICS says what it means)
+DTYPES = {0: "f32", 1: "f16", 2: "u8"}
+NUMERICS = {0: "FP32 FFMA2 accumulation, two-level summation",
+            1: "3-term FP16 split (mma.sync m16n8k16), FP32 accumulation, two-level summation",
+            2: "23-bit fixed-point factors as three u8 limbs (tcgen05.mma kind::i8), exact S32 accumulation, "
+               "one FP32 rounding per voxel; max |gpu - oracle| <= 6e-7 of max (DESIGN.md §5)"}
 CONFIG_INDEX = {"tiny": 0, "dengue": 1, "social": 2, "ornith": 3, "stress": 4}
 # oracle sample sizes for the cpu_baseline / reference legs (about 10-30 s of host work)
 ORACLE_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 600000, "ornith": 1000000, "stress": 150000}
@@ -462,7 +468,8 @@ def gpu_main(args, w, rank, world, local_rank):
         result = {
             "metric": METRIC, "value": C_total / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": DTYPES[info["engine"]],
+            "numerics": NUMERICS[info["engine"]], "data": "synthetic",
             "config": config_dict(w, info, dict(variant_config(variant), **{
                 "contributions": C_total, "ms_per_grid": ms_max / len(outs),
                 "parallelism": ("x-slab x%d" if xsplit else "time-slab x%d") % world,
