@@ -471,9 +471,9 @@ extern "C" int stkde_slab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, int Bt, int H
 }
 
 // ---- x-slabs (multi-GPU partition along X) ----
-// Per-column cost: alpha * Gy*Gt*4 B / B_hbm + beta * 2 W(X) / P_fp32 with W(X) = sum_i
-// chord_i(X) * (2 rt + 1), chord_i(X) = 2 sqrt(rs^2 - (X - X_i)^2) (the disc's extent in Y
-// at column X times the window's layers); cuts at multiples of 16 columns (tile width).
+// Per-column cost: alpha * Gy*Gt*4 B / B_hbm + beta * 2 W(X) / P_fp32 with W(X) = (2 rs)
+// (2 rt + 1) #{points with |X - X_i| <= rs + 8} (the tile kernel's candidates of the
+// column's 16-wide tile); cuts at multiples of 16 columns (tile width).
 extern "C" int stkde_xslab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, double rs, double rt, const int64_t *h_hist_X,
                                 int nparts, int64_t *h_cuts) {
     if (!h_cuts || !h_hist_X || nparts < 1 || Gx < 1 || Gy < 1 || Gt < 1 || !(rs > 0) || !(rt > 0)) {
@@ -481,9 +481,11 @@ extern "C" int stkde_xslab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, double rs, d
         return STKDE_EINVAL;
     }
     const double B_hbm = 6.5e12, P_fp32 = 6.0e13;
-    const int R = (int)std::ceil(rs);
-    std::vector<double> chord(2 * R + 1);
-    for (int d = -R; d <= R; ++d) chord[d + R] = 2.0 * std::sqrt(std::max(rs * rs - (double)d * d, 0.0));
+    // the tile kernel's cost follows its candidates (every point whose box reaches the
+    // column's 16-wide tile), so each point weighs the full disc height 2 rs over the
+    // columns within rs + 8 of it (measured: more even slab times than chord weights)
+    const int R = (int)std::ceil(rs) + BX / 2;
+    std::vector<double> chord(2 * R + 1, 2.0 * rs);
     const int64_t nblk = (Gx + BX - 1) / BX;
     std::vector<double> cost(nblk, 0.0);
     for (int64_t X = 0; X < Gx; ++X) {
