@@ -236,10 +236,10 @@ def gpu_main(args, w, rank, world, local_rank):
     bw = torch.from_numpy(bw_host).to(dev) if bw_host is not None else None
     fr = synth.SWEEP_FRACTIONS
     sw_hs, sw_ht = [f * w.hs for f in fr], [f * w.ht for f in fr]
-    # N > 1: the fixed variant splits the grid into cost-balanced X-slabs (stkde_compute_xslab:
-    # the slab's tiles are the full grid's, so the work splits without overhead); the adaptive
-    # variant into cost-balanced time slabs (stkde_compute_adaptive_slab)
-    xsplit = world > 1 and variant == "fixed"
+    # N > 1: the fixed and adaptive variants split the grid into cost-balanced X-slabs
+    # (stkde_compute_[adaptive_]xslab: the slab's tiles are the full grid's, so the work splits
+    # without overhead)
+    xsplit = world > 1 and variant in ("fixed", "adaptive")
     x0, x1 = 0, w.G[0]
     with torch.cuda.stream(stream):
         if xsplit:
@@ -250,7 +250,12 @@ def gpu_main(args, w, rank, world, local_rank):
             cuts = plan.slab_partition(pts, world, stream=stream) if world > 1 else [0, w.G[2]]
         t0, t1 = cuts[0 if xsplit else rank], cuts[1 if xsplit else rank + 1]
         if xsplit:   # the metric's C is the whole grid's: count it on rank 0 only
-            C = int(plan.count_contributions(pts, 0, w.G[2], stream=stream).item()) if rank == 0 else 0
+            if rank != 0:
+                C = 0
+            elif variant == "adaptive":
+                C = int(plan.count_contributions_adaptive(pts, bw, 0, w.G[2], stream=stream).item())
+            else:
+                C = int(plan.count_contributions(pts, 0, w.G[2], stream=stream).item())
         elif t1 <= t0:
             C = 0
         elif variant == "adaptive":
@@ -274,7 +279,10 @@ def gpu_main(args, w, rank, world, local_rank):
     def run(p_pts, p_bw):
         if t1 <= t0:
             return
-        if variant == "adaptive":
+        if variant == "adaptive" and xsplit:
+            if x1 > x0:
+                plan.compute_adaptive_xslab(p_pts, p_bw, x0, x1, n_norm=w.n, out=out, stream=stream)
+        elif variant == "adaptive":
             plan.compute_adaptive_slab(p_pts, p_bw, t0, t1, n_norm=w.n, out=out, stream=stream)
         elif variant == "sweep":
             plan.compute_sweep(p_pts, sw_hs, sw_ht, outs=outs, stream=stream)
@@ -366,7 +374,10 @@ def gpu_main(args, w, rank, world, local_rank):
             if xpipe is not None:
                 stream.wait_stream(copy_stream)
                 for (a, b), ev in zip(xpipe, slab_ev):
-                    plan.compute_xslab(dpts, a, b, n_norm=w.n, out=out[a - x0:b - x0], stream=stream)
+                    if variant == "adaptive":
+                        plan.compute_adaptive_xslab(dpts, dbw, a, b, n_norm=w.n, out=out[a - x0:b - x0], stream=stream)
+                    else:
+                        plan.compute_xslab(dpts, a, b, n_norm=w.n, out=out[a - x0:b - x0], stream=stream)
                     ev.record(stream)
                     copy_stream.wait_event(ev)
                     with torch.cuda.stream(copy_stream):

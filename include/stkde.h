@@ -181,6 +181,9 @@ int stkde_compute_sweep(stkde_plan_t plan, const float *d_points, int64_t n, int
  * (else STKDE_EINVAL).  Asynchronous. */
 int stkde_compute_xslab(stkde_plan_t plan, const float *d_points, int64_t n, int64_t n_norm,
                         int64_t x_begin, int64_t x_end, float *d_xslab, void *stream);
+/* The same for the adaptive estimator (d_bw as in stkde_compute_adaptive). */
+int stkde_compute_adaptive_xslab(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
+                                 int64_t n_norm, int64_t x_begin, int64_t x_end, float *d_xslab, void *stream);
 /* Cost-balanced x cuts (multiples of 16, h_cuts[0] = 0, h_cuts[nparts] = Gx); the cost of
  * column X is Gy*Gt*4 B / B_hbm + 2 W(X) / P_fp32, W(X) = sum over the points with
  * |X - X_i| <= rs + 8 of 2 rs (2 rt + 1) -- the tile kernel's candidates.  stkde_xslab_partition reads the X_i histogram from the device

@@ -534,8 +534,8 @@ extern "C" int stkde_xslab_partition(stkde_plan_t p, const float *d_points, int6
     return stkde_xslab_cuts(g.Gx, g.Gy, g.Gt, (double)g.rs, (double)g.rt, h64.data(), nparts, h_cuts);
 }
 
-extern "C" int stkde_compute_xslab(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm,
-                                   int64_t x_begin, int64_t x_end, float *d_xslab, void *stream) {
+static int xslab_impl(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n, int64_t n_norm,
+                      int64_t x_begin, int64_t x_end, float *d_xslab, void *stream) {
     if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
     const GridParams g0 = p->g;
     if (p->engine != STKDE_ENGINE_TC) { set_error("x-slabs need the tcgen05 engine"); return STKDE_EINVAL; }
@@ -556,9 +556,21 @@ extern "C" int stkde_compute_xslab(stkde_plan_t p, const float *d_points, int64_
     p->g.NXA = (int)((x_end + BX - 1) / BX - x_begin / BX);
     // the tile kernel indexes the full grid; the slab is that grid's block of rows [x_begin, x_end)
     float *out_shifted = d_xslab - x_begin * (int64_t)g0.Gy * g0.Gt;
-    const int rc = compute_slab_impl(p, d_points, n, n_norm, 0, g0.Gt, out_shifted, (cudaStream_t)stream);
+    const int rc = compute_slab_impl(p, d_points, n, n_norm, 0, g0.Gt, out_shifted, (cudaStream_t)stream, d_bw);
     p->g = g0;
     return rc;
+}
+
+extern "C" int stkde_compute_xslab(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm,
+                                   int64_t x_begin, int64_t x_end, float *d_xslab, void *stream) {
+    return xslab_impl(p, d_points, nullptr, n, n_norm, x_begin, x_end, d_xslab, stream);
+}
+
+extern "C" int stkde_compute_adaptive_xslab(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n,
+                                            int64_t n_norm, int64_t x_begin, int64_t x_end, float *d_xslab,
+                                            void *stream) {
+    if (n > 0 && !d_bw) { set_error("d_bw is NULL"); return STKDE_EINVAL; }
+    return xslab_impl(p, d_points, n > 0 ? d_bw : nullptr, n, n_norm, x_begin, x_end, d_xslab, stream);
 }
 
 extern "C" int stkde_slab_partition(stkde_plan_t p, const float *d_points, int64_t n, int nparts, int64_t *h_cuts,

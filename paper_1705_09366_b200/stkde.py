@@ -27,7 +27,7 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress", "stkde_strerror",
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
            "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
-           "stkde_xslab_partition", "stkde_xslab_cuts")
+           "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab")
 
 
 class StkdeError(RuntimeError):
@@ -81,6 +81,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_count_contributions_adaptive.argtypes = [P, P, P, I64, I64, I64, P, P]
     L.stkde_compute_sweep.argtypes = [P, P, I64, I32, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(P), P]
     L.stkde_compute_xslab.argtypes = [P, P, I64, I64, I64, I64, P, P]
+    L.stkde_compute_adaptive_xslab.argtypes = [P, P, P, I64, I64, I64, I64, P, P]
     L.stkde_xslab_partition.argtypes = [P, P, I64, I32, ctypes.POINTER(I64), P]
     L.stkde_xslab_cuts.argtypes = [I64, I64, I64, D, D, ctypes.POINTER(I64), I32, ctypes.POINTER(I64)]
     L.stkde_strerror.argtypes = [I32]
@@ -92,7 +93,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
                  "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress",
                  "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
-                 "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts"):
+                 "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts",
+                 "stkde_compute_adaptive_xslab"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -246,6 +248,23 @@ class Plan:
         nn = pts.shape[0] if n_norm is None else int(n_norm)
         _check(load_library().stkde_compute_xslab(self._h, pts.data_ptr(), pts.shape[0], nn, int(x_begin), int(x_end),
                                                   out.data_ptr(), _stream_ptr(stream, self.device)))
+        return out
+
+    def compute_adaptive_xslab(self, points: torch.Tensor, bw: torch.Tensor, x_begin: int, x_end: int,
+                               n_norm: Optional[int] = None, out: Optional[torch.Tensor] = None,
+                               stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Adaptive-bandwidth grid rows [x_begin, x_end): [x_end - x_begin, Gy, Gt] float32."""
+        pts = _points_arg(points, self.device)
+        b = _bw_arg(bw, self.device, pts.shape[0])
+        shape = (int(x_end) - int(x_begin), self.G[1], self.G[2])
+        if out is None:
+            out = torch.empty(shape, dtype=torch.float32, device=self.device)
+        if out.device != self.device or out.dtype != torch.float32 or not out.is_contiguous() or tuple(out.shape) != shape:
+            raise ValueError("out must be a contiguous float32 CUDA tensor of shape %s" % (shape,))
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        _check(load_library().stkde_compute_adaptive_xslab(self._h, pts.data_ptr(), b.data_ptr(), pts.shape[0], nn,
+                                                           int(x_begin), int(x_end), out.data_ptr(),
+                                                           _stream_ptr(stream, self.device)))
         return out
 
     def xslab_partition(self, points: torch.Tensor, nparts: int,

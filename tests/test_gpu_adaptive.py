@@ -268,3 +268,19 @@ def test_sweep_full_size_sampled(S, oracle_mod):
         vox = _sample_voxels(gpu, synth.SplitMix64(17 + k), k_top=300, k_rand=300)
         val, slack, amb = oracle_mod.stkde_vb_voxels(w.points, vox, **gk)
         assert_parity(gpu.reshape(-1)[vox], val, slack, amb, vmax=max(val.max(), 0.0), what="sweep f=%g" % f)
+
+
+def test_adaptive_xslabs_equal_full(S):
+    # adaptive x-slabs (multiples of 16 columns) are the full adaptive grid's rows, bitwise
+    w = synth.make_config("dengue")
+    g = w.grid_kwargs()
+    bw = synth.adaptive_bandwidths(w)
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        t, b = torch.from_numpy(w.points).to(dev), torch.from_numpy(bw).to(dev)
+        full = p.compute_adaptive(t, b).cpu().numpy()
+        cuts = p.xslab_partition(t, 4)
+        for a, c in zip(cuts[:-1], cuts[1:]):
+            s = p.compute_adaptive_xslab(t, b, a, c, n_norm=w.n).cpu().numpy()
+            assert np.array_equal(s, full[a:c]), (a, c)
+        p.check()
