@@ -205,6 +205,14 @@ int stkde_compute_sharded(stkde_plan_t *plans, int ndev,
                           float *const *d_slabs, int64_t *h_cuts,
                           int root, float *d_full_grid, void *const *streams);
 
+/* X-slab counterpart of stkde_compute_sharded: d_slabs[d] receives rows
+ * [h_cuts[d], h_cuts[d+1]) (float32 [rows][Gy][Gt]); cuts from stkde_xslab_partition
+ * on plans[0] when h_cuts[0] < 0; the optional gather is one peer copy per device
+ * (each x-slab is a contiguous block of the full grid).  Same stream/asynchrony rules. */
+int stkde_compute_sharded_x(stkde_plan_t *plans, int ndev, const float *const *d_points, int64_t n,
+                            float *const *d_slabs, int64_t *h_cuts, int root, float *d_full_grid,
+                            void *const *streams);
+
 /* Synchronises the plan's device; returns STKDE_ENONFINITE if any point of
  * a previous call had a non-finite coordinate (and clears the flag). */
 int stkde_plan_check(stkde_plan_t plan);

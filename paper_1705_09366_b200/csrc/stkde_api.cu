@@ -646,6 +646,48 @@ extern "C" int stkde_compute_sharded(stkde_plan_t *plans, int ndev, const float 
     return STKDE_OK;
 }
 
+// X-slab variant: device d computes rows [h_cuts[d], h_cuts[d+1]); a slab is a contiguous
+// block of the full layout, so the gather is one peer copy per device into the root's grid.
+extern "C" int stkde_compute_sharded_x(stkde_plan_t *plans, int ndev, const float *const *d_points, int64_t n,
+                                       float *const *d_slabs, int64_t *h_cuts, int root, float *d_full_grid,
+                                       void *const *streams) {
+    if (!plans || ndev < 1 || !d_points || !d_slabs || !h_cuts || !streams) { set_error("bad arguments"); return STKDE_EINVAL; }
+    for (int d = 0; d < ndev; ++d)
+        if (!plans[d]) { set_error("plans[%d] is NULL", d); return STKDE_EINVAL; }
+    if (h_cuts[0] < 0) {
+        int rc = stkde_xslab_partition(plans[0], d_points[0], n, ndev, h_cuts, streams[0]);
+        if (rc) return rc;
+    }
+    for (int d = 0; d < ndev; ++d) {
+        if (h_cuts[d + 1] <= h_cuts[d]) continue;   // empty slab
+        int rc = stkde_compute_xslab(plans[d], d_points[d], n, n, h_cuts[d], h_cuts[d + 1], d_slabs[d], streams[d]);
+        if (rc) return rc;
+    }
+    if (d_full_grid) {
+        if (root < 0 || root >= ndev) { set_error("root out of range"); return STKDE_EINVAL; }
+        stkde_plan_s *pr = plans[root];
+        CK(cudaSetDevice(pr->device));
+        cudaStream_t rs = (cudaStream_t)streams[root];
+        const size_t row = (size_t)pr->g.Gy * pr->g.Gt * sizeof(float);
+        for (int d = 0; d < ndev; ++d) {
+            if (h_cuts[d + 1] <= h_cuts[d]) continue;
+            if (streams[d] != streams[root]) {
+                cudaEvent_t ev;
+                CK(cudaSetDevice(plans[d]->device));
+                CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                CK(cudaEventRecord(ev, (cudaStream_t)streams[d]));
+                CK(cudaSetDevice(pr->device));
+                CK(cudaStreamWaitEvent(rs, ev, 0));
+                cudaEventDestroy(ev);
+            }
+            char *dst = reinterpret_cast<char *>(d_full_grid) + (size_t)h_cuts[d] * row;
+            const size_t bytes = (size_t)(h_cuts[d + 1] - h_cuts[d]) * row;
+            CK(cudaMemcpyPeerAsync(dst, pr->device, d_slabs[d], plans[d]->device, bytes, rs));
+        }
+    }
+    return STKDE_OK;
+}
+
 extern "C" int stkde_plan_check(stkde_plan_t p) {
     if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
     CK(cudaSetDevice(p->device));

@@ -27,7 +27,7 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress", "stkde_strerror",
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
            "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
-           "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab")
+           "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x")
 
 
 class StkdeError(RuntimeError):
@@ -82,6 +82,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_compute_sweep.argtypes = [P, P, I64, I32, ctypes.POINTER(D), ctypes.POINTER(D), ctypes.POINTER(P), P]
     L.stkde_compute_xslab.argtypes = [P, P, I64, I64, I64, I64, P, P]
     L.stkde_compute_adaptive_xslab.argtypes = [P, P, P, I64, I64, I64, I64, P, P]
+    L.stkde_compute_sharded_x.argtypes = [ctypes.POINTER(P), I32, ctypes.POINTER(P), I64, ctypes.POINTER(P),
+                                          ctypes.POINTER(I64), I32, P, ctypes.POINTER(P)]
     L.stkde_xslab_partition.argtypes = [P, P, I64, I32, ctypes.POINTER(I64), P]
     L.stkde_xslab_cuts.argtypes = [I64, I64, I64, D, D, ctypes.POINTER(I64), I32, ctypes.POINTER(I64)]
     L.stkde_strerror.argtypes = [I32]
@@ -94,7 +96,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress",
                  "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
                  "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts",
-                 "stkde_compute_adaptive_xslab"):
+                 "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -355,8 +357,9 @@ class Plan:
 
 def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs: Sequence[torch.Tensor],
                     cuts: Optional[Sequence[int]] = None, root: int = -1,
-                    full: Optional[torch.Tensor] = None, streams=None) -> list:
-    """Single-process multi-device driver (stkde_compute_sharded); returns the cuts used."""
+                    full: Optional[torch.Tensor] = None, streams=None, axis: str = "t") -> list:
+    """Single-process multi-device driver (stkde_compute_sharded, or stkde_compute_sharded_x for
+    axis="x": slabs[d] = rows [cuts[d], cuts[d+1]) as [rows, Gy, Gt]); returns the cuts used."""
     L = load_library()
     nd = len(plans)
     P = ctypes.c_void_p
@@ -368,8 +371,8 @@ def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs
     if streams is None:
         streams = [torch.cuda.current_stream(p.device) for p in plans]
     hs = (P * nd)(*[int(s.cuda_stream) for s in streams])
-    _check(L.stkde_compute_sharded(hp, nd, hpts, pts[0].shape[0], hsl, hc, int(root),
-                                   None if full is None else full.data_ptr(), hs))
+    fn = L.stkde_compute_sharded_x if axis == "x" else L.stkde_compute_sharded
+    _check(fn(hp, nd, hpts, pts[0].shape[0], hsl, hc, int(root), None if full is None else full.data_ptr(), hs))
     return [int(c) for c in hc]
 
 

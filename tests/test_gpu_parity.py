@@ -361,3 +361,25 @@ def test_sharded_driver_axes(S, axis):
         cuts = d.cuts
         d.close()
     assert torch.equal(assemble(slabs, cuts, w.G, axis=axis), full)
+
+
+def test_sharded_x_single_process_equals_full(S):
+    # stkde_compute_sharded_x with every "device" mapped to GPU 0: x-slabs + the per-device
+    # peer copies into the root's grid reproduce the full grid bitwise; cuts from the device
+    w = synth.make_config("dengue")
+    g = w.grid_kwargs()
+    dev = torch.device("cuda", 0)
+    t = torch.from_numpy(w.points).to(dev)
+    plans = [S.Plan(max_n=w.n, device=0, **g) for _ in range(3)]
+    try:
+        full_ref = plans[0].compute(t).clone()
+        cuts = plans[0].xslab_partition(t, 3)
+        slabs = [torch.empty((cuts[i + 1] - cuts[i], g["Gy"], g["Gt"]), device=dev) for i in range(3)]
+        full = torch.full_like(full_ref, -1.0)
+        used = S.compute_sharded(plans, [t] * 3, slabs, root=0, full=full, axis="x")
+        torch.cuda.synchronize()
+        assert used == cuts
+        assert torch.equal(full, full_ref)
+    finally:
+        for p in plans:
+            p.close()
