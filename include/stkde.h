@@ -30,9 +30,11 @@
  *     only; kernel faults surface at the caller's next synchronisation.
  *   - A plan must not be used concurrently from two streams.
  *   - Results are deterministic: identical inputs give bitwise identical
- *     grids, and a time slab computed by stkde_compute_slab with a slab
- *     boundary that is a multiple of the plan's tile height Bt is bitwise
- *     equal to the same layers of the full-grid result.
+ *     grids.  A time slab (stkde_compute_slab) or x-slab (stkde_compute_xslab)
+ *     is bitwise equal to the same block of the full-grid result: with the
+ *     tcgen05 engine for any boundary (exact integer accumulation, one rounding
+ *     per voxel), with the FP32 engines for time-slab boundaries that are
+ *     multiples of the tile height Bt.
  *   - Return codes: STKDE_OK (0) or a negative STKDE_E* value; the message
  *     of the most recent error on the calling thread is stkde_last_error().
  */
