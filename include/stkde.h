@@ -160,6 +160,28 @@ int stkde_compute_adaptive_slab(stkde_plan_t plan, const float *d_points, const 
 int stkde_count_contributions_adaptive(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
                                        int64_t t_begin, int64_t t_end, int64_t *d_count, void *stream);
 
+/* ---- FP64 output (SPEC.md:48-54 keeps the volume in FP64) ----
+ * The same density as stkde_compute / stkde_compute_slab / stkde_compute_adaptive_slab
+ * (same arguments, slab and normalisation rules), written as float64
+ * [Gx][Gy][t_end - t_begin] (T innermost; d_grid / d_slab on the plan's device,
+ * fully overwritten).  Every (point, voxel) term is evaluated in FP64 with the IEEE
+ * operation sequence of Alg. 1 -- voxel centre
+ * x0 + (X + 0.5) sres, gates sqrt(dx^2 + dy^2) < hs and |dt| <= ht, the printed or
+ * classical kernels -- without contraction, so the gate decisions
+ * and each term equal a plain FP64 evaluation of the definition; the per-voxel sum
+ * runs in a fixed order (home bucket, then ascending point index), the sum is divided
+ * by n hs^2 ht at the end (adaptive: each term by hs_i^2 ht_i, the sum by n).
+ * Deterministic; slabs are bitwise equal to the full grid's layers.  FP64-pipe bound
+ * (DESIGN.md §3.8): an accuracy option, not the throughput path.  Any engine for
+ * the fixed bandwidth; the adaptive form needs the tcgen05 engine (else STKDE_EINVAL).
+ * Asynchronous; the non-finite / bandwidth flags as for the FP32 calls. */
+int stkde_compute_f64(stkde_plan_t plan, const float *d_points, int64_t n, double *d_grid, void *stream);
+int stkde_compute_slab_f64(stkde_plan_t plan, const float *d_points, int64_t n, int64_t n_norm,
+                           int64_t t_begin, int64_t t_end, double *d_slab, void *stream);
+int stkde_compute_adaptive_slab_f64(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
+                                    int64_t n_norm, int64_t t_begin, int64_t t_end, double *d_slab,
+                                    void *stream);
+
 /* ---- Multi-bandwidth sweep (Fig. 1, PAPER.md:135-146:
  * the same events viewed at several bandwidths; the Lb/Hb/VHb instances of
  * PAPER.md:651-653) ----

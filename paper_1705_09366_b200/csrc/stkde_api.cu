@@ -356,6 +356,55 @@ extern "C" int stkde_compute_adaptive(stkde_plan_t p, const float *d_points, con
     return compute_slab_impl(p, d_points, n, n, 0, p->g.Gt, d_grid, (cudaStream_t)stream, n > 0 ? d_bw : nullptr);
 }
 
+// ---- FP64-output option (stkde_tile_f64.cu) ----
+static int compute_f64_impl(stkde_plan_s *p, const float *d_points, const float *d_bw, int64_t n, int64_t n_norm,
+                            int64_t t_begin, int64_t t_end, double *d_out, cudaStream_t st) {
+    const GridParams &g = p->g;
+    p->last_own_launches = 0;
+    p->last_cub_calls = 0;
+    if (d_bw && p->engine != STKDE_ENGINE_TC) {
+        set_error("adaptive bandwidths need the tcgen05 engine (H_s <= 120, STKDE_ENGINE unset or 2)");
+        return STKDE_EINVAL;
+    }
+    if (n < 0 || n_norm < 0) { set_error("n must be >= 0"); return STKDE_EINVAL; }
+    if (n > p->max_n) { set_error("n = %lld exceeds the plan's max_n = %lld", (long long)n, (long long)p->max_n); return STKDE_ECAPACITY; }
+    if (t_begin < 0 || t_end > g.Gt || t_begin >= t_end) { set_error("slab [t_begin, t_end) must satisfy 0 <= t_begin < t_end <= Gt"); return STKDE_EINVAL; }
+    if (!d_out || (n > 0 && !d_points)) { set_error("NULL device pointer"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(p->device));
+    if (n == 0 || n_norm == 0) {   // empty point set -> zeros, no division
+        CK(cudaMemsetAsync(d_out, 0, (size_t)g.Gx * g.Gy * (t_end - t_begin) * sizeof(double), st));
+        return STKDE_OK;
+    }
+    BwScope scope(p, d_bw);
+    int rc = launch_binning(p, d_points, n, st, t_begin, t_end);
+    if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    // Alg. 1 divides the sum by n hs^2 ht; adaptive: terms carry 1/(hs_i^2 ht_i), the sum 1/n
+    const double den = d_bw ? (double)n_norm : (double)n_norm * (g.hs * g.hs) * g.ht;
+    rc = launch_tile_f64(p, d_points, d_bw, t_begin, t_end, den, d_out, st);
+    if (rc) { set_error("FP64 tile kernel launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    return STKDE_OK;
+}
+
+extern "C" int stkde_compute_f64(stkde_plan_t p, const float *d_points, int64_t n, double *d_grid, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    return compute_f64_impl(p, d_points, nullptr, n, n, 0, p->g.Gt, d_grid, (cudaStream_t)stream);
+}
+
+extern "C" int stkde_compute_slab_f64(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm,
+                                      int64_t t_begin, int64_t t_end, double *d_slab, void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    return compute_f64_impl(p, d_points, nullptr, n, n_norm, t_begin, t_end, d_slab, (cudaStream_t)stream);
+}
+
+extern "C" int stkde_compute_adaptive_slab_f64(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n,
+                                               int64_t n_norm, int64_t t_begin, int64_t t_end, double *d_slab,
+                                               void *stream) {
+    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    if (n > 0 && !d_bw) { set_error("d_bw is NULL"); return STKDE_EINVAL; }
+    return compute_f64_impl(p, d_points, n > 0 ? d_bw : nullptr, n, n_norm, t_begin, t_end, d_slab,
+                            (cudaStream_t)stream);
+}
+
 extern "C" int stkde_compute_adaptive_slab(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n,
                                            int64_t n_norm, int64_t t_begin, int64_t t_end, float *d_slab,
                                            void *stream) {

@@ -252,5 +252,7 @@ size_t tile_tc_smem_bytes(int BT);
 int tile_tc_occupancy(int BT, int kernel, int *ctas_per_sm);
 int launch_tile_tc(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float cscale, float *out,
                    cudaStream_t st);
+int launch_tile_f64(stkde_plan_s *p, const float *d_points, const float *d_bw, int64_t t_begin, int64_t t_end,
+                    double den, double *out, cudaStream_t st);
 void set_error(const char *fmt, ...);
 }  // namespace stkde

@@ -27,7 +27,8 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress", "stkde_strerror",
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
            "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
-           "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x")
+           "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x",
+           "stkde_compute_f64", "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64")
 
 
 class StkdeError(RuntimeError):
@@ -86,6 +87,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                           ctypes.POINTER(I64), I32, P, ctypes.POINTER(P)]
     L.stkde_xslab_partition.argtypes = [P, P, I64, I32, ctypes.POINTER(I64), P]
     L.stkde_xslab_cuts.argtypes = [I64, I64, I64, D, D, ctypes.POINTER(I64), I32, ctypes.POINTER(I64)]
+    L.stkde_compute_f64.argtypes = [P, P, I64, P, P]
+    L.stkde_compute_slab_f64.argtypes = [P, P, I64, I64, I64, I64, P, P]
+    L.stkde_compute_adaptive_slab_f64.argtypes = [P, P, P, I64, I64, I64, I64, P, P]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
@@ -96,7 +100,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress",
                  "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
                  "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts",
-                 "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x"):
+                 "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x", "stkde_compute_f64",
+                 "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64"):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -226,6 +231,29 @@ class Plan:
                                                            _stream_ptr(stream, self.device)))
         return out
 
+    # -- FP64 output (include/stkde.h) --
+    def compute_f64(self, points: torch.Tensor, t_begin: int = 0, t_end: Optional[int] = None,
+                    n_norm: Optional[int] = None, bw: Optional[torch.Tensor] = None,
+                    out: Optional[torch.Tensor] = None, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """float64 [Gx, Gy, t_end - t_begin]: every term in FP64 with Alg. 1's operation
+        sequence; bw = per-point (hs_i, ht_i) for the adaptive estimator (None: fixed)."""
+        pts = _points_arg(points, self.device)
+        t_end = self.G[2] if t_end is None else int(t_end)
+        ts = t_end - int(t_begin)
+        if out is None:
+            out = torch.empty((self.G[0], self.G[1], max(ts, 0)), dtype=torch.float64, device=self.device)
+        self._check_out(out, ts, torch.float64)
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        L, st = load_library(), _stream_ptr(stream, self.device)
+        if bw is None:
+            _check(L.stkde_compute_slab_f64(self._h, pts.data_ptr(), pts.shape[0], nn, int(t_begin), t_end,
+                                            out.data_ptr(), st))
+        else:
+            b = _bw_arg(bw, self.device, pts.shape[0])
+            _check(L.stkde_compute_adaptive_slab_f64(self._h, pts.data_ptr(), b.data_ptr(), pts.shape[0], nn,
+                                                     int(t_begin), t_end, out.data_ptr(), st))
+        return out
+
     def count_contributions_adaptive(self, points: torch.Tensor, bw: torch.Tensor, t_begin: int = 0,
                                      t_end: Optional[int] = None,
                                      stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -297,11 +325,11 @@ class Plan:
                                                   _stream_ptr(stream, self.device)))
         return list(outs)
 
-    def _check_out(self, out, ts):
-        if out.device != self.device or out.dtype != torch.float32 or not out.is_contiguous() \
+    def _check_out(self, out, ts, dtype=torch.float32):
+        if out.device != self.device or out.dtype != dtype or not out.is_contiguous() \
                 or tuple(out.shape) != (self.G[0], self.G[1], ts):
-            raise ValueError("out must be a contiguous float32 CUDA tensor of shape %s"
-                             % ((self.G[0], self.G[1], ts),))
+            raise ValueError("out must be a contiguous %s CUDA tensor of shape %s"
+                             % (dtype, (self.G[0], self.G[1], ts)))
 
     def slab_partition(self, points: torch.Tensor, nparts: int,
                        stream: Optional[torch.cuda.Stream] = None) -> list:
