@@ -27,6 +27,9 @@ a bounded sample of the same workload (rank 0 only; other ranks exit 0).
   sweep     stkde_compute_sweep over (f hs, f ht), f in stkde_synth.SWEEP_FRACTIONS:
             one binning, one grid per bandwidth; C = sum over the grids.  N = 1 only.
             `separate_ms` times the same grids as separate plans + computes.
+  f64       the FP64-output option (stkde_compute_slab_f64): every
+            term in FP64 with Alg. 1's operation sequence, float64 grid; roofline against
+            the FP64 pipe.
 """
 import argparse
 import json
@@ -47,6 +50,7 @@ import stkde_synth as synth  # noqa: E402
 METRIC = "point-voxel contributions/sec"
 UNIT = "contributions/s"
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x 2 x max SM clock
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12    # 37.2: SMs x FP64 lanes x 2 x max SM clock
 ENGINES = {0: "SIMT FP32 FFMA2", 1: "mma.sync m16n8k16 3xFP16", 2: "tcgen05.mma kind::i8, exact S32"}
 KERNELS = {0: "stkde::k_tile<Bt=%d>", 1: "stkde::k_tile_mma<Bt=%d>", 2: "stkde::k_tile_tc<Bt=%d>"}
 # the arithmetic type of the contraction (not a precision claim; NUMERICS says what it means)
@@ -55,6 +59,8 @@ NUMERICS = {0: "FP32 FFMA2 accumulation, two-level summation",
             1: "3-term FP16 split (mma.sync m16n8k16), FP32 accumulation, two-level summation",
             2: "23-bit fixed-point factors as three u8 limbs (tcgen05.mma kind::i8), exact S32 accumulation, "
                "one FP32 rounding per voxel; max |gpu - oracle| <= 6e-7 of max (DESIGN.md §5)"}
+NUMERICS_F64 = ("FP64 gates and factors with Alg. 1's operation sequence, fma accumulation in FP64, float64 grid; "
+                "|gpu - oracle| <= 2 (n + 2) 2^-53 f per voxel, exact support (DESIGN.md §3.8)")
 CONFIG_INDEX = {"tiny": 0, "dengue": 1, "social": 2, "ornith": 3, "stress": 4}
 # oracle sample sizes for the cpu_baseline / reference legs (about 10-30 s of host work)
 ORACLE_SAMPLE = {"tiny": 2000, "dengue": 11000, "social": 600000, "ornith": 1000000, "stress": 150000}
@@ -196,6 +202,9 @@ def variant_config(variant):
         return {"variant": "adaptive bandwidth (DESIGN.md R15): stkde_synth.adaptive_bandwidths, lambda in [0.25, 1]"}
     if variant == "sweep":
         return {"variant": "multi-bandwidth sweep: (f hs, f ht), f in %s, one binning" % (list(synth.SWEEP_FRACTIONS),)}
+    if variant == "f64":
+        return {"variant": "FP64 output (stkde_compute_slab_f64): FP64 gates, factors and fma accumulation, "
+                           "float64 grid (DESIGN.md §3.8)"}
     return {}
 
 
@@ -271,8 +280,9 @@ def gpu_main(args, w, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(Ct)
     C_total = int(Ct.item())
-    out = (torch.empty((max(x1 - x0, 1), w.G[1], w.G[2]), dtype=torch.float32, device=dev) if xsplit else
-           torch.empty((w.G[0], w.G[1], max(t1 - t0, 1)), dtype=torch.float32, device=dev))
+    odt = torch.float64 if variant == "f64" else torch.float32
+    out = (torch.empty((max(x1 - x0, 1), w.G[1], w.G[2]), dtype=odt, device=dev) if xsplit else
+           torch.empty((w.G[0], w.G[1], max(t1 - t0, 1)), dtype=odt, device=dev))
     outs = [out] + [torch.empty_like(out) for _ in fr[1:]] if variant == "sweep" else [out]
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -286,6 +296,8 @@ def gpu_main(args, w, rank, world, local_rank):
             plan.compute_adaptive_slab(p_pts, p_bw, t0, t1, n_norm=w.n, out=out, stream=stream)
         elif variant == "sweep":
             plan.compute_sweep(p_pts, sw_hs, sw_ht, outs=outs, stream=stream)
+        elif variant == "f64":
+            plan.compute_f64(p_pts, t0, t1, n_norm=w.n, out=out, stream=stream)
         elif xsplit:
             if x1 > x0:
                 plan.compute_xslab(p_pts, x0, x1, n_norm=w.n, out=out, stream=stream)
@@ -363,7 +375,7 @@ def gpu_main(args, w, rank, world, local_rank):
         copy_stream = torch.cuda.Stream(dev)
         slab_ev = [torch.cuda.Event() for _ in pipe]
     if host_outs is None:
-        host_outs = [torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory() for _ in outs]
+        host_outs = [torch.empty(tuple(out.shape), dtype=out.dtype).pin_memory() for _ in outs]
     barrier()
     eb, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):
@@ -403,7 +415,8 @@ def gpu_main(args, w, rank, world, local_rank):
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
     h2d = (w.points.nbytes + (bw_host.nbytes if bw_host is not None else 0)) * world
-    d2h = w.G[0] * w.G[1] * w.G[2] * 4 * len(outs)
+    esz = out.element_size()
+    d2h = w.G[0] * w.G[1] * w.G[2] * esz * len(outs)
 
     # sweep: the same grids as separate plans + computes (what the one binning saves)
     separate_ms = None
@@ -431,11 +444,17 @@ def gpu_main(args, w, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel (the tile kernel) ----
     (hbm_peak, hbm_src), (bf16_peak, bf16_src) = peaks()
-    grid_bytes = (x1 - x0) * w.G[1] * (t1 - t0) * 4 * len(outs)
+    grid_bytes = (x1 - x0) * w.G[1] * (t1 - t0) * esz * len(outs)
     t_hbm = grid_bytes / (hbm_peak * 1e9)
     C_rank = C_total / world if xsplit else C       # x-slabs: per-rank work ~ C / N (cost-balanced cuts)
     t_fp32 = 2.0 * C_rank / (FP32_NOMINAL_TFLOPS * 1e12)
-    if t_fp32 >= t_hbm:
+    if variant == "f64" and 2.0 * C_rank / (FP64_NOMINAL_TFLOPS * 1e12) >= t_hbm:
+        ach = 2.0 * C_rank / (kernel_ms * 1e-3) / 1e12
+        roof = {"bound": "alu", "achieved": ach, "peak": FP64_NOMINAL_TFLOPS, "unit": "TFLOP/s (FP64)",
+                "frac": ach / FP64_NOMINAL_TFLOPS,
+                "peak_source": "derived: 148 SMs x 64 FP64 lanes x 2 FLOP x 1.965 GHz (DESIGN.md §3.8); "
+                               "tools/fma_peak measured 36.5 TFLOP/s DFMA"}
+    elif t_fp32 >= t_hbm and variant != "f64":
         ach = 2.0 * C_rank / (kernel_ms * 1e-3) / 1e12
         roof = {"bound": "alu", "achieved": ach, "peak": FP32_NOMINAL_TFLOPS, "unit": "TFLOP/s",
                 "frac": ach / FP32_NOMINAL_TFLOPS,
@@ -446,10 +465,11 @@ def gpu_main(args, w, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
                 "peak_source": hbm_src}
     roof["traffic"] = profile_traffic(w.name, info["engine"], variant)
-    roof["kernel"] = KERNELS[info["engine"]] % info["Bt"]
+    roof["kernel"] = "stkde::k_tile_f64" if variant == "f64" else KERNELS[info["engine"]] % info["Bt"]
     roof["kernel_ms"] = kernel_ms_max
     roof["algorithmic"] = {"flops": 2 * C_rank, "bytes": grid_bytes,
-                           "per_unit": "2 FLOP per contribution (one FMA acc += K_s*K_t), 4 B per voxel written once"}
+                           "per_unit": "2 FLOP per contribution (one FMA acc += K_s*K_t), %d B per voxel written once"
+                                       % esz}
     # the tensor pipe's own roofline (tcgen05 engine): int8 ops the kernel issued per launch
     # (7 MMAs of 128 x N x 32 per k-block, 2 ops per MAC) against the dense int8 peak
     # = 2 x the measured dense bf16 peak (the guide's nominal int8:bf16 ratio on sm_100)
@@ -479,8 +499,9 @@ def gpu_main(args, w, rank, world, local_rank):
         result = {
             "metric": METRIC, "value": C_total / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": DTYPES[info["engine"]],
-            "numerics": NUMERICS[info["engine"]], "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if variant == "f64" else DTYPES[info["engine"]],
+            "numerics": NUMERICS_F64 if variant == "f64" else NUMERICS[info["engine"]], "data": "synthetic",
             "config": config_dict(w, info, dict(variant_config(variant), **{
                 "contributions": C_total, "ms_per_grid": ms_max / len(outs),
                 "parallelism": ("x-slab x%d" if xsplit else "time-slab x%d") % world,
@@ -498,7 +519,7 @@ def gpu_main(args, w, rank, world, local_rank):
             "clocks": clk.summary(),
             "roofline": roof,
             "roofline_tensor": roof_tc,
-            "engine": ENGINES[info["engine"]],
+            "engine": "FP64 gather tiles (stkde_tile_f64.cu)" if variant == "f64" else ENGINES[info["engine"]],
             "cpu_baseline": cpu,
         }
         if variant != "fixed":
@@ -533,7 +554,7 @@ def main():
     ap.add_argument("--config", default="stress", choices=sorted(CONFIG_INDEX))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--variant", default="fixed", choices=["fixed", "adaptive", "sweep"])
+    ap.add_argument("--variant", default="fixed", choices=["fixed", "adaptive", "sweep", "f64"])
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))

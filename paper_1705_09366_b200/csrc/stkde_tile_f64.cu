@@ -209,12 +209,18 @@ int launch_tile_f64(stkde_plan_s *p, const float *d_points, const float *d_bw, i
     const int64_t nz = (t_end - t_begin + F64_TL - 1) / F64_TL;
     if (nz > 65535) { set_error("FP64 slab too deep (%lld layers)", (long long)(t_end - t_begin)); return STKDE_EINVAL; }
     const dim3 grid((unsigned)g.NTX, (unsigned)g.NTY, (unsigned)nz);
+    const bool timed = p->timing && p->tev_used < p->tev_cap;
+    if (timed) cudaEventRecord(p->tev[2 * p->tev_used], st);
     if (d_bw)
         k_tile_f64<true><<<grid, ncol, 0, st>>>(g, p->rec_sorted, p->vals_out, p->bucket_begin, d_points, d_bw,
                                                     (int)t_begin, (int)t_end, den, out);
     else
         k_tile_f64<false><<<grid, ncol, 0, st>>>(g, p->rec_sorted, p->vals_out, p->bucket_begin, d_points,
                                                      nullptr, (int)t_begin, (int)t_end, den, out);
+    if (timed) {
+        cudaEventRecord(p->tev[2 * p->tev_used + 1], st);
+        p->tev_used += 1;
+    }
     p->last_own_launches += 1;
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }

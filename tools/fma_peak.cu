@@ -1,5 +1,6 @@
-// FP32 FMA-pipe microbenchmark: FFMA (scalar) and FFMA2 (packed f32x2) with
-// independent accumulator chains, to measure the SIMT FP32 roofline on B200.
+// FMA-pipe microbenchmark: FFMA (scalar), FFMA2 (packed f32x2) and DFMA (FP64) with
+// independent accumulator chains, to measure the SIMT FP32 roofline and the FP64
+// roofline of the FP64-output option on B200.
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -34,9 +35,24 @@ __global__ void k_ffma2(float *out, float a, float b, int iters) {
     if (s == 12345.f) out[0] = s;
 }
 
+template <int NACC>
+__global__ void k_dfma(double *out, double a, double b, int iters) {
+    double acc[NACC];
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] = threadIdx.x * 1e-3 + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < NACC; ++i) acc[i] = fma(acc[i], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) s += acc[i];
+    if (s == 12345.) out[0] = s;
+}
+
 int main() {
     float *d;
-    cudaMalloc(&d, 4);
+    cudaMalloc(&d, 8);
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaEvent_t e0, e1;
@@ -60,6 +76,13 @@ int main() {
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms, e0, e1);
         printf("FFMA2: %.1f TFLOP/s (%.3f ms)\n", fl / ms / 1e9, ms);
+        k_dfma<16><<<blocks, threads>>>((double *)d, 0.999, 1e-3, 100);
+        cudaEventRecord(e0);
+        k_dfma<16><<<blocks, threads>>>((double *)d, 0.999, 1e-3, iters / 4);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("DFMA : %.2f TFLOP/s (%.3f ms)\n", fl / 4 / ms / 1e9, ms);
     }
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
