@@ -96,6 +96,7 @@ CASES = [
     ("classical", 600, G(33, 47, 35, hs=4.0, ht=3.0), 1, True),
     ("world_units", 700, G(50, 40, 30, res=0.37, hs=1.5, ht=1.2, origin=(1000.5, -2000.25, 30.0), tres=0.41), 0, True),
     ("big_disc", 200, G(80, 70, 40, hs=30.0, ht=6.0), 0, False),
+    ("deep_window", 400, G(40, 36, 90, hs=5.0, ht=18.0), 0, True),   # H_t >= 16: 32-layer blocks
     ("one_voxel_grid", 50, G(1, 1, 1, hs=2.0, ht=2.0), 0, False),
 ]
 
@@ -137,8 +138,9 @@ def test_f64_stress_full_size_sampled(S, oracle_mod):
     print("stress sampled: max rel %.3e over %d voxels" % (rel, len(vox)))
 
 
-def test_f64_slabs_bitwise_and_deterministic(S, oracle_mod):
-    g = G(40, 36, 150, hs=6.0, ht=9.0)
+@pytest.mark.parametrize("ht", [9.0, 20.0], ids=["tl16", "tl32"])
+def test_f64_slabs_bitwise_and_deterministic(S, oracle_mod, ht):
+    g = G(40, 36, 150, hs=6.0, ht=ht)
     pts = make_points(700, g, True, seed=41)
     full = run_f64(S, pts, **g)
     again = run_f64(S, pts, **g)
