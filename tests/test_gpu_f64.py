@@ -121,21 +121,32 @@ def test_f64_config_full_parity(S, oracle_mod, name):
     print("%s: max rel %.3e" % (name, rel))
 
 
-def test_f64_stress_full_size_sampled(S, oracle_mod):
-    # BASELINE.json's stress config at full size: sampled voxels (the densest,
-    # random support voxels, random voxels) against Alg. 1 voxel by voxel.
-    w = synth.make_config("stress")
+@pytest.mark.parametrize("name", ["ornith", "stress"])
+def test_f64_full_size_sampled(S, oracle_mod, name):
+    # BASELINE.json's largest configs at full size (ornith: 16-layer blocks, stress: 32):
+    # sampled voxels -- the densest, random support voxels, random voxels, chosen on the
+    # device so the float64 grid never leaves it -- against Alg. 1 voxel by voxel.
+    w = synth.make_config(name)
     g = w.grid_kwargs()
-    gpu = run_f64(S, w.points, **g).reshape(-1)
-    r = synth.SplitMix64(23)
-    top = np.argpartition(gpu, -300)[-300:]
-    nz = np.flatnonzero(gpu > 0)
-    pick = nz[(r.uniform01(300) * len(nz)).astype(np.int64) % len(nz)]
-    rnd = (r.uniform01(100) * gpu.size).astype(np.int64) % gpu.size
-    vox = np.unique(np.concatenate([top, pick, rnd]))
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        pts = torch.from_numpy(w.points).to(dev)
+        out = p.compute_f64(pts).reshape(-1)
+        torch.cuda.synchronize()
+        p.check()
+        r = synth.SplitMix64(23)
+        top = torch.topk(out, 300).indices
+        cand = torch.from_numpy((r.uniform01(200000) * out.numel()).astype(np.int64) % out.numel()).to(dev)
+        sup = cand[out[cand] > 0][:300]
+        rnd = torch.from_numpy((r.uniform01(100) * out.numel()).astype(np.int64) % out.numel()).to(dev)
+        vox = torch.unique(torch.cat([top, sup, rnd]))
+        gv = out[vox].cpu().numpy()
+        vox = vox.cpu().numpy()
+        del out
     val, _, _ = oracle_mod.stkde_vb_voxels(w.points, vox, **g)
-    rel = assert_f64_parity(gpu[vox], val, w.n, what="stress")
-    print("stress sampled: max rel %.3e over %d voxels" % (rel, len(vox)))
+    assert (val > 0).sum() >= 300
+    rel = assert_f64_parity(gv, val, w.n, what=name)
+    print("%s sampled: max rel %.3e over %d voxels" % (name, rel, len(vox)))
 
 
 @pytest.mark.parametrize("ht", [9.0, 20.0], ids=["tl16", "tl32"])
@@ -178,6 +189,18 @@ def test_f64_adaptive_parity(S, oracle_mod):
     print("adaptive: max rel %.3e" % rel)
     sl = run_f64(S, pts, bw=bw, t_begin=7, t_end=30, **g)
     assert np.array_equal(sl.view(np.uint64), gpu[:, :, 7:30].view(np.uint64))
+
+
+def test_f64_adaptive_classical_world_units(S, oracle_mod):
+    g = G(50, 40, 30, res=0.37, hs=1.5, ht=1.2, origin=(1000.5, -2000.25, 30.0), tres=0.41)
+    pts = make_points(500, g, True, seed=91)
+    r = synth.SplitMix64(92)
+    v = r.uniform01(2 * len(pts)).reshape(-1, 2)
+    cap = np.array([np.float32(1.5), np.nextafter(np.float32(1.2), np.float32(0))], np.float32)
+    bw = np.minimum(((0.3 + 0.7 * v) * np.array([1.5, 1.2])).astype(np.float32), cap)
+    gpu = run_f64(S, pts, kernel=1, bw=bw, **g)
+    ref = oracle_mod.stkde_pb_adaptive(pts, bw, kernel=1, with_ambiguity=False, **g)
+    assert_f64_parity(gpu, ref.vol, len(pts), what="adaptive classical world units")
 
 
 def test_f64_edge_cases(S):
