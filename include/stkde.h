@@ -71,7 +71,7 @@ enum {
  * §3.5.  TC: the same contraction on 5th-generation tensor cores (tcgen05.mma
  * kind::i8, 23-bit fixed-point factors split into three 8-bit limbs, exact S32
  * accumulation in TMEM; M = 128 columns of a 16x8-column tile, A generated
- * into TMEM) -- DESIGN.md §3.6.  Hs > 120 falls back to TENSOR.  All engines compute the same sums
+ * into TMEM) -- DESIGN.md §3.5.  Hs > 120 falls back to TENSOR.  All engines compute the same sums
  * within the parity tolerance; they differ in speed only. */
 enum { STKDE_ENGINE_SIMT = 0, STKDE_ENGINE_TENSOR = 1, STKDE_ENGINE_TC = 2 };
 
@@ -81,8 +81,9 @@ typedef struct stkde_plan_s *stkde_plan_t;
  * sizes sres/tres > 0, grid Gx,Gy,Gt >= 1 and bandwidths hs, ht > 0 are in
  * world units (H_s = ceil(hs/sres), H_t = ceil(ht/tres)).
  * `max_n` bounds the point count of later calls and sizes the device
- * workspace, so compute calls never allocate.  The tile height Bt is chosen
- * from H_t (16, 32 or 64); read it back with stkde_plan_info.  Writes the
+ * workspace, so compute calls never allocate.  The tile shape depends on the
+ * engine (tcgen05: 16 x 8 columns x Bt = 64 or 128 layers; legacy engines: 16 x 16
+ * columns x Bt = 16, 32 or 64 from H_t); read it back with stkde_plan_info.  Writes the
  * plan to *out.  Errors: STKDE_EINVAL (message names the field),
  * STKDE_ENOMEM, STKDE_ECUDA. */
 int stkde_plan_create(stkde_plan_t *out, int device,
@@ -135,6 +136,13 @@ int stkde_slab_cuts(int64_t Gx, int64_t Gy, int64_t Gt, int Bt, int Ht, double r
 int stkde_count_contributions(stkde_plan_t plan, const float *d_points, int64_t n,
                               int64_t t_begin, int64_t t_end, int64_t *d_count,
                               void *stream);
+/* The same count restricted to the voxels of rows [x_begin, x_end) and layers
+ * [t_begin, t_end) (an x-slab's or a time slab's own contributions: the per-rank work of
+ * a sharded run).  0 <= x_begin < x_end <= Gx, 0 <= t_begin < t_end <= Gt, else
+ * STKDE_EINVAL.  Asynchronous. */
+int stkde_count_contributions_box(stkde_plan_t plan, const float *d_points, int64_t n,
+                                  int64_t x_begin, int64_t x_end, int64_t t_begin, int64_t t_end,
+                                  int64_t *d_count, void *stream);
 
 /* ---- Adaptive bandwidth (reading R15) ----
  * PAPER.md:1060-1062 names "a bandwidth that adapts to the density of
@@ -237,8 +245,23 @@ int stkde_compute_sharded_x(stkde_plan_t *plans, int ndev, const float *const *d
                             float *const *d_slabs, int64_t *h_cuts, int root, float *d_full_grid,
                             void *const *streams);
 
-/* Synchronises the plan's device; returns STKDE_ENONFINITE if any point of
- * a previous call had a non-finite coordinate (and clears the flag). */
+/* Conditions raised on the device by earlier calls (bit mask, see stkde_plan_check_flags). */
+enum {
+    STKDE_FLAG_NONFINITE = 1,   /* a point had a non-finite coordinate (skipped)                 */
+    STKDE_FLAG_WORKLIST = 2,    /* internal work-list capacity exceeded (a library bug)          */
+    STKDE_FLAG_BANDWIDTH = 4    /* an adaptive call had a per-point bandwidth outside the plan's
+                                   range (skipped)                                               */
+};
+
+/* Synchronises the plan's device, writes every condition raised since the last check to
+ * *flags (STKDE_FLAG_* bits, 0 = none) and clears them.  Errors: STKDE_EINVAL (NULL),
+ * STKDE_ECUDA. */
+int stkde_plan_check_flags(stkde_plan_t plan, uint32_t *flags);
+
+/* Synchronises the plan's device and clears the flags; returns STKDE_OK if none was
+ * raised, else the code of the most severe one (STKDE_ECUDA for a work-list overflow,
+ * then STKDE_ENONFINITE, then STKDE_EBANDWIDTH) with stkde_last_error() naming EVERY
+ * raised condition. */
 int stkde_plan_check(stkde_plan_t plan);
 
 /* Plan facts: tile shape, H, workspace bytes, number of kernels the last
@@ -267,21 +290,10 @@ int stkde_plan_kernel_ms(stkde_plan_t plan, double *ms_total, int64_t *launches)
 
 /* Instrumentation of the tcgen05 engine: since the last call,
  * the sum over issued k-blocks of the MMA width N (each k-block issues 7
- * tcgen05.mma kind::i8 of 128 x N x 32) and the number of k-blocks; both are
+ * tcgen05.mma kind::i8 of 128 x N x 32) and the number of k-blocks (accumulated in
+ * registers, two atomics per generator team when the persistent CTA exits); both are
  * reset.  Synchronises the device.  Zero for the other engines. */
 int stkde_plan_mma_stats(stkde_plan_t plan, int64_t *mma_columns, int64_t *kblocks);
-
-/* Development diagnostics of the tcgen05 engine: with STKDE_TC_PROF=1 in the
- * environment at plan creation, the tile kernel accumulates clock64 phase
- * totals of one thread per role (generator teams: [0..10], loader: [16..23];
- * layout in stkde_tile_tc.cu); this copies the 32 u64 counters to out32 and
- * resets them.  Synchronises the device. */
-int stkde_plan_tc_profile(stkde_plan_t plan, uint64_t *out32);
-
-/* Development diagnostics: buf = device-accessible (e.g. pinned host) array of
- * num_sms * 32 uint32; the tcgen05 kernel's warps publish their protocol state
- * (tag << 24 | step) in it while running.  NULL disables. */
-int stkde_plan_debug_progress(stkde_plan_t plan, void *buf);
 
 /* Human-readable message for a return code / the last error of this thread. */
 const char *stkde_strerror(int code);

@@ -7,7 +7,9 @@ CUDA sources (csrc/), the in-tree build (build.py), the ctypes binding
 (stkde.py) and the time-slab multi-GPU driver (sharded.py).
 """
 from .stkde import (KERNEL_CLASSICAL, KERNEL_PRINTED, EXPORTS, LIB_PATH, Plan, StkdeError,  # noqa: F401
-                    STKDE_EBANDWIDTH, STKDE_EINVAL, STKDE_ENONFINITE, compute_sharded, load_library, slab_cuts, stkde, xslab_cuts)
+                    STKDE_EBANDWIDTH, STKDE_EINVAL, STKDE_ENONFINITE, FLAG_BANDWIDTH, FLAG_NONFINITE,
+                    FLAG_WORKLIST, compute_sharded, load_library, slab_cuts, stkde, xslab_cuts)
 
 __all__ = ["Plan", "StkdeError", "stkde", "compute_sharded", "load_library", "slab_cuts", "KERNEL_PRINTED",
-           "KERNEL_CLASSICAL", "EXPORTS", "LIB_PATH", "STKDE_EBANDWIDTH", "STKDE_EINVAL", "STKDE_ENONFINITE", "xslab_cuts"]
+           "KERNEL_CLASSICAL", "EXPORTS", "LIB_PATH", "STKDE_EBANDWIDTH", "STKDE_EINVAL", "STKDE_ENONFINITE", "xslab_cuts",
+           "FLAG_NONFINITE", "FLAG_WORKLIST", "FLAG_BANDWIDTH"]

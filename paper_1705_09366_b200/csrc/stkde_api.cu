@@ -19,6 +19,9 @@
 #include <vector>
 
 #include "stkde_internal.cuh"
+#if STKDE_TC_DIAG
+#include "stkde_diag.h"
+#endif
 
 namespace stkde {
 static thread_local char g_err[512] = "";
@@ -158,7 +161,20 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     // 16533 points before 2^31.
     // (measured: the largest chunk is fastest -- fewer split tiles and partial passes; the
     // LPT order already starts the heaviest items first)
-    if (p->engine == STKDE_ENGINE_TC) chunk = std::min<int64_t>(env_int("STKDE_CHUNK", 16384), 16384);
+    // the slot budget (STKDE_SLOT_MB) still bounds the split-tile partial slots: the chunk is the
+    // larger of the request and the budget-derived minimum, capped at the S32 limit; if even
+    // the cap cannot meet the budget the plan is refused (max_n too large for the budget)
+    if (p->engine == STKDE_ENGINE_TC) {
+        const int64_t need = (2 * cand_bound + slot_budget - 1) / slot_budget;
+        if (need > 16384) {
+            set_error("max_n = %lld needs %lld-candidate work items for the %d MiB split-slot budget "
+                      "(STKDE_SLOT_MB), above the 16384-candidate S32 limit: lower max_n or raise STKDE_SLOT_MB",
+                      (long long)max_n, (long long)need, env_int("STKDE_SLOT_MB", 1024));
+            free(p);
+            return STKDE_EINVAL;
+        }
+        chunk = std::min<int64_t>(std::max<int64_t>(env_int("STKDE_CHUNK", 16384), need), 16384);
+    }
     chunk = std::min<int64_t>(chunk, (int64_t)1 << 30);
     p->chunk = (int)chunk;
     p->max_items = p->ntiles + cand_bound / chunk + 1;
@@ -327,12 +343,14 @@ extern "C" int stkde_compute_slab(stkde_plan_t p, const float *d_points, int64_t
 }
 
 static int count_impl(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n, int64_t t_begin,
-                      int64_t t_end, int64_t *d_count, void *stream) {
+                      int64_t t_end, int64_t *d_count, void *stream, int64_t x_begin = 0, int64_t x_end = -1) {
     if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+    if (x_end < 0) x_end = p->g.Gx;
     if (n < 0 || (n > 0 && !d_points) || !d_count) { set_error("bad points/count arguments"); return STKDE_EINVAL; }
     if (t_begin < 0 || t_end > p->g.Gt || t_begin >= t_end) { set_error("bad slab"); return STKDE_EINVAL; }
+    if (x_begin < 0 || x_end > p->g.Gx || x_begin >= x_end) { set_error("bad x range"); return STKDE_EINVAL; }
     CK(cudaSetDevice(p->device));
-    int rc = launch_count(p, d_points, n, t_begin, t_end, d_count, (cudaStream_t)stream, d_bw);
+    int rc = launch_count(p, d_points, n, t_begin, t_end, d_count, (cudaStream_t)stream, d_bw, x_begin, x_end);
     if (rc) set_error("count launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return rc;
 }
@@ -340,6 +358,12 @@ static int count_impl(stkde_plan_t p, const float *d_points, const float *d_bw, 
 extern "C" int stkde_count_contributions(stkde_plan_t p, const float *d_points, int64_t n, int64_t t_begin,
                                          int64_t t_end, int64_t *d_count, void *stream) {
     return count_impl(p, d_points, nullptr, n, t_begin, t_end, d_count, stream);
+}
+
+extern "C" int stkde_count_contributions_box(stkde_plan_t p, const float *d_points, int64_t n, int64_t x_begin,
+                                             int64_t x_end, int64_t t_begin, int64_t t_end, int64_t *d_count,
+                                             void *stream) {
+    return count_impl(p, d_points, nullptr, n, t_begin, t_end, d_count, stream, x_begin, x_end);
 }
 
 extern "C" int stkde_count_contributions_adaptive(stkde_plan_t p, const float *d_points, const float *d_bw, int64_t n,
@@ -739,17 +763,32 @@ extern "C" int stkde_compute_sharded_x(stkde_plan_t *plans, int ndev, const floa
     return STKDE_OK;
 }
 
-extern "C" int stkde_plan_check(stkde_plan_t p) {
-    if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
+extern "C" int stkde_plan_check_flags(stkde_plan_t p, uint32_t *flags) {
+    if (!p || !flags) { set_error("NULL argument"); return STKDE_EINVAL; }
     CK(cudaSetDevice(p->device));
     CK(cudaDeviceSynchronize());
-    int flags = 0;
-    CK(cudaMemcpy(&flags, p->counters + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    int f = 0;
+    CK(cudaMemcpy(&f, p->counters + 1, sizeof(int), cudaMemcpyDeviceToHost));
     CK(cudaMemset(p->counters + 1, 0, sizeof(int)));
-    if (flags & 2) { set_error("internal work-list capacity exceeded"); return STKDE_ECUDA; }
-    if (flags & 1) { set_error("non-finite point coordinate(s) were skipped"); return STKDE_ENONFINITE; }
-    if (flags & 4) { set_error("point(s) with a bandwidth outside (0, plan hs] x (0, plan ht] were skipped"); return STKDE_EBANDWIDTH; }
+    *flags = (uint32_t)f & (STKDE_FLAG_NONFINITE | STKDE_FLAG_WORKLIST | STKDE_FLAG_BANDWIDTH);
     return STKDE_OK;
+}
+
+extern "C" int stkde_plan_check(stkde_plan_t p) {
+    uint32_t flags = 0;
+    const int rc = stkde_plan_check_flags(p, &flags);
+    if (rc) return rc;
+    if (!flags) return STKDE_OK;
+    // every raised condition is named in the message; the code is the most severe one
+    char msg[400] = "";
+    if (flags & STKDE_FLAG_WORKLIST) strcat(msg, "internal work-list capacity exceeded; ");
+    if (flags & STKDE_FLAG_NONFINITE) strcat(msg, "non-finite point coordinate(s) were skipped; ");
+    if (flags & STKDE_FLAG_BANDWIDTH) strcat(msg, "point(s) with a bandwidth outside (0, plan hs] x (0, plan ht] were skipped; ");
+    msg[strlen(msg) - 2] = 0;
+    set_error("%s", msg);
+    if (flags & STKDE_FLAG_WORKLIST) return STKDE_ECUDA;
+    if (flags & STKDE_FLAG_NONFINITE) return STKDE_ENONFINITE;
+    return STKDE_EBANDWIDTH;
 }
 
 extern "C" int stkde_plan_info(stkde_plan_t p, stkde_plan_info_t *info) {
@@ -807,6 +846,9 @@ extern "C" int stkde_plan_mma_stats(stkde_plan_t p, int64_t *mma_columns, int64_
     return STKDE_OK;
 }
 
+#if STKDE_TC_DIAG
+// development diagnostics (paper_1705_09366_b200/csrc/stkde_diag.h): only in a
+// -DSTKDE_TC_DIAG=1 build (scripts/build_variant.py), not part of the product ABI
 extern "C" int stkde_plan_tc_profile(stkde_plan_t p, uint64_t *out32) {
     if (!p || !out32) { set_error("NULL argument"); return STKDE_EINVAL; }
     CK(cudaSetDevice(p->device));
@@ -823,6 +865,7 @@ extern "C" int stkde_plan_debug_progress(stkde_plan_t p, void *buf) {
     p->debug_progress = buf;
     return STKDE_OK;
 }
+#endif
 
 extern "C" const char *stkde_strerror(int code) {
     switch (code) {

@@ -232,7 +232,7 @@ __global__ void k_items(const uint32_t *__restrict__ lval, const uint64_t *__res
 
 // Exact contribution count: one warp per point (adaptive: the point's own bandwidths).
 __global__ void k_count(const float *__restrict__ pts, int64_t n, GridParams gp, int64_t t_begin, int64_t t_end,
-                        unsigned long long *__restrict__ out, const float *__restrict__ bwin) {
+                        unsigned long long *__restrict__ out, const float *__restrict__ bwin, int x_begin, int x_end) {
     __shared__ unsigned long long part[32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -248,8 +248,8 @@ __global__ void k_count(const float *__restrict__ pts, int64_t n, GridParams gp,
             for (int Y = y0 + lane; Y <= y1; Y += 32) {
                 int lo, hi;
                 row_chord(g, r, Y, &lo, &hi);
-                lo = max(lo, 0);
-                hi = min(hi, g.Gx - 1);
+                lo = max(lo, x_begin);
+                hi = min(hi, x_end - 1);
                 cols += max(hi - lo + 1, 0);
             }
             int t0 = (int)max((int64_t)r.T - g.Ht, t_begin), t1 = (int)min((int64_t)r.T + g.Ht, t_end - 1);
@@ -361,11 +361,12 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
 }
 
 int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_begin, int64_t t_end,
-                 int64_t *d_count, cudaStream_t st, const float *d_bw) {
+                 int64_t *d_count, cudaStream_t st, const float *d_bw, int64_t x_begin, int64_t x_end) {
     cudaMemsetAsync(d_count, 0, sizeof(int64_t), st);
     if (n > 0)
         k_count<<<nblk(n * 32, 256), 256, 0, st>>>(d_points, n, p->g, t_begin, t_end,
-                                                   reinterpret_cast<unsigned long long *>(d_count), d_bw);
+                                                   reinterpret_cast<unsigned long long *>(d_count), d_bw,
+                                                   (int)x_begin, (int)x_end);
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }
 

@@ -236,7 +236,8 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,
                 float *out, cudaStream_t st);
 int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_begin,
-                 int64_t t_end, int64_t *d_count, cudaStream_t st, const float *d_bw = nullptr);
+                 int64_t t_end, int64_t *d_count, cudaStream_t st, const float *d_bw, int64_t x_begin,
+                 int64_t x_end);
 int launch_hist_t(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
 int launch_hist_x(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st);
 int launch_gather(const float *slab, int64_t Gx, int64_t Gy, int64_t Gt, int64_t t0, int64_t t1,

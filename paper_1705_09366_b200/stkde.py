@@ -18,13 +18,15 @@ LIB_PATH = os.path.join(_PKG, "libstkde.so")
 
 STKDE_OK, STKDE_EINVAL, STKDE_ENOMEM, STKDE_ECUDA, STKDE_ECAPACITY, STKDE_ENONFINITE = 0, -1, -2, -3, -4, -5
 STKDE_EBANDWIDTH = -6
+FLAG_NONFINITE, FLAG_WORKLIST, FLAG_BANDWIDTH = 1, 2, 4
 KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
 
 # Exported entry points of include/stkde.h (checked by tests/test_abi.py).
 EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_compute_slab",
            "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
-           "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress", "stkde_strerror",
+           "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_check_flags", "stkde_count_contributions_box",
+           "stkde_strerror",
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
            "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
            "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x",
@@ -75,8 +77,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_enable_kernel_timing.argtypes = [P, I32]
     L.stkde_plan_kernel_ms.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(I64)]
     L.stkde_plan_mma_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
-    L.stkde_plan_tc_profile.argtypes = [P, ctypes.POINTER(ctypes.c_uint64)]
-    L.stkde_plan_debug_progress.argtypes = [P, P]
+    L.stkde_plan_check_flags.argtypes = [P, ctypes.POINTER(ctypes.c_uint32)]
+    L.stkde_count_contributions_box.argtypes = [P, P, I64, I64, I64, I64, I64, P, P]
+    # development diagnostics: exported only by a -DSTKDE_TC_DIAG=1 build (csrc/stkde_diag.h)
+    DIAG = ("stkde_plan_tc_profile", "stkde_plan_debug_progress")
+    if hasattr(L, DIAG[0]):
+        L.stkde_plan_tc_profile.argtypes = [P, ctypes.POINTER(ctypes.c_uint64)]
+        L.stkde_plan_debug_progress.argtypes = [P, P]
     L.stkde_compute_adaptive.argtypes = [P, P, P, I64, P, P]
     L.stkde_compute_adaptive_slab.argtypes = [P, P, P, I64, I64, I64, I64, P, P]
     L.stkde_count_contributions_adaptive.argtypes = [P, P, P, I64, I64, I64, P, P]
@@ -97,11 +104,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     for name in ("stkde_plan_create", "stkde_compute", "stkde_compute_slab", "stkde_slab_partition", "stkde_slab_cuts",
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
-                 "stkde_plan_mma_stats", "stkde_plan_tc_profile", "stkde_plan_debug_progress",
+                 "stkde_plan_mma_stats", "stkde_plan_check_flags", "stkde_count_contributions_box",
                  "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
                  "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts",
                  "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x", "stkde_compute_f64",
-                 "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64"):
+                 "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64") + (DIAG if hasattr(L, DIAG[0]) else ()):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -349,9 +356,26 @@ class Plan:
             out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
 
+    def count_contributions_box(self, points: torch.Tensor, x_begin: int, x_end: int, t_begin: int = 0,
+                                t_end: Optional[int] = None,
+                                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        """Exact C restricted to rows [x_begin, x_end) and layers [t_begin, t_end) (async)."""
+        pts = _points_arg(points, self.device)
+        out = torch.empty(1, dtype=torch.int64, device=self.device)
+        _check(load_library().stkde_count_contributions_box(
+            self._h, pts.data_ptr(), pts.shape[0], int(x_begin), int(x_end), int(t_begin),
+            int(self.G[2] if t_end is None else t_end), out.data_ptr(), _stream_ptr(stream, self.device)))
+        return out
+
     # -- diagnostics --
     def check(self):
         _check(load_library().stkde_plan_check(self._h))
+
+    def check_flags(self) -> int:
+        """Every condition raised since the last check (STKDE_FLAG_* bits), then cleared."""
+        f = ctypes.c_uint32(0)
+        _check(load_library().stkde_plan_check_flags(self._h, ctypes.byref(f)))
+        return int(f.value)
 
     def info(self) -> dict:
         i = PlanInfo()

@@ -56,6 +56,10 @@ SMALL = [
     ("big_disc", 200, G(80, 70, 40, hs=30.0, ht=6.0), 0, False),
     ("one_voxel_grid", 50, G(1, 1, 1, hs=2.0, ht=2.0), 0, False),
     ("thin_slab", 400, G(64, 64, 3, hs=4.0, ht=1.0), 0, True),
+    # classical kernel on Bt = 128 tiles (Gt > 64): small disc (H_s < 16, the PF = 1
+    # loader instantiation) and large disc (H_s >= 16)
+    ("classical_bt128_small", 900, G(45, 37, 150, hs=5.0, ht=6.0), 1, True),
+    ("classical_bt128_large", 250, G(70, 60, 140, hs=18.0, ht=9.0), 1, False),
 ]
 
 
@@ -104,30 +108,6 @@ def test_config_full_parity(S, oracle_mod, name, engine):
     rel = assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=name)
     assert C == ref.contributions
     print("%s: max |gpu-oracle|/max = %.3e, C = %d, tile %s" % (name, rel, C, (info["Bx"], info["By"], info["Bt"])))
-
-
-def _sample_voxels(gpu, rng, k_top=600, k_rand=600):
-    flat = gpu.reshape(-1)
-    top = np.argpartition(flat, -k_top)[-k_top:]
-    nz = np.flatnonzero(flat > 0)
-    pick = nz[(rng.uniform01(k_rand) * len(nz)).astype(np.int64) % len(nz)]
-    rnd = (rng.uniform01(200) * flat.size).astype(np.int64) % flat.size
-    return np.unique(np.concatenate([top, pick, rnd]))
-
-
-@pytest.mark.parametrize("name", ["ornith", "stress"])
-def test_config_full_size_sampled(S, oracle_mod, name):
-    # BASELINE.json full sizes, the bench.py launch configuration: sampled
-    # voxels (the densest ones, random support voxels, random voxels) against
-    # Alg. 1 evaluated voxel by voxel, plus the exact contribution count.
-    w = synth.make_config(name)
-    g = w.grid_kwargs()
-    gpu, C, _ = run_gpu(S, w.points, **g)
-    vox = _sample_voxels(gpu, synth.SplitMix64(11))
-    val, slack, amb = oracle_mod.stkde_vb_voxels(w.points, vox, **g)
-    vmax = max(val.max(), 0.0)
-    assert_parity(gpu.reshape(-1)[vox], val, slack, amb, vmax=vmax, what=name)
-    assert C == oracle_mod.contributions(w.points, **g)
 
 
 def test_determinism_and_slabs(S, engine):
@@ -383,3 +363,22 @@ def test_sharded_x_single_process_equals_full(S):
     finally:
         for p in plans:
             p.close()
+
+
+@pytest.mark.parametrize("case", [c for c in SMALL if c[0].startswith("classical_bt128")], ids=lambda c: c[0])
+def test_classical_bt128_slabs(S, oracle_mod, case):
+    # the classical kernel on Bt = 128 tiles (both loader instantiations) through
+    # the slab calls: every slab equals the full grid's layers bitwise, the full grid the oracle
+    name, n, g, kid, clustered = case
+    pts = make_points(n, g, clustered, seed=len(name))
+    dev = torch.device("cuda", 0)
+    with S.Plan(max_n=len(pts), kernel=kid, device=0, **g) as p:
+        assert p.info()["Bt"] == 128
+        t = torch.from_numpy(pts).to(dev)
+        full = p.compute(t).cpu().numpy()
+        for t0, t1 in ((0, 64), (32, 96), (5, 133), (128, g["Gt"]), (0, g["Gt"])):
+            s = p.compute_slab(t, t0, t1, n_norm=len(pts)).cpu().numpy()
+            assert np.array_equal(s, full[:, :, t0:t1]), (t0, t1)
+        p.check()
+    ref = oracle_mod.stkde_pb(pts, kernel=kid, **g)
+    assert_parity(full, ref.vol, ref.slack, ref.amb, what=name)

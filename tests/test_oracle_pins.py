@@ -268,3 +268,67 @@ def test_tiny_config_full(oracle_mod):
     vb = oracle_mod.stkde_vb(w.points[:400], **g)
     pb = oracle_mod.stkde_pb(w.points[:400], **g)
     assert np.array_equal(vb.vol, pb.vol)
+
+
+# ----------------------------------------------------------------- slack ---
+@pytest.mark.parametrize("kid", [0, 1])
+def test_slack_closed_form(oracle_mod, kid):
+    # Reading R10/R11: slack(voxel) = sum over the voxel's ambiguous pairs
+    # of |k_s k_t| / (n hs^2 ht); 0 on unambiguous voxels.  One point at the voxel centre
+    # (10.5, 10.5, 10.5), hs = 5, ht = 2 (n = 1):
+    #  * columns at integer offsets (3, 4) / (4, 3) lie exactly on the circle d = hs
+    #    (Pythagorean): ambiguous, outside the strict gate, k_s(0.6, 0.8) =
+    #    pi/2 (0.4)^2 (0.2)^2 = 0.0064 pi/2 printed, 2/pi (1 - 0.36 - 0.64) = 0 classical
+    #    (up to the FP64 rounding of 0.6 and 0.8);
+    #  * columns (5, 0) / (0, 5): ambiguous, k_s(1, 0) = 0;
+    #  * layers dt = +-2 = ht: inside the inclusive temporal gate, ambiguous, k_t(1) = 0.
+    # So the slack of a (3,4)-type voxel at layer offset dt is k_s(0.6,0.8) k_t(|dt|/2) / 50,
+    # the sum over the grid is 8 k_s(0.6,0.8) (k_t(0) + 2 k_t(0.5)) / 50 = 8 k_s 1.125 / 50,
+    # and the ambiguous voxels are the 12 circle columns x 5 layers plus the strict disc
+    # interior (Gauss count) x 2 edge layers.  Catches slack = 0 everywhere (a dropped
+    # slack), slack added to unambiguous voxels, a missing 1/(n hs^2 ht), or an ambiguity
+    # test on the wrong side of the gate.
+    g = grid(G=(21, 21, 21), res=1.0, hs=5.0, ht=2.0)
+    r = oracle_mod.stkde_pb(np.array([[10.5, 10.5, 10.5]], np.float32), kernel=kid, **g)
+    ks34 = (math.pi / 2) * 0.4 ** 2 * 0.2 ** 2 if kid == 0 else 0.0
+    kt = {0: 0.75, 1: 0.75 * 0.25 if kid == 0 else 0.75 * 0.75, 2: 0.0}
+    for dx, dy in ((3, 4), (-4, 3), (4, -3), (-3, -4)):
+        for dt in (-2, -1, 0, 1, 2):
+            v = (10 + dx, 10 + dy, 10 + dt)
+            assert r.amb[v] == 1 and r.vol[v] == 0
+            assert r.slack[v] == pytest.approx(ks34 * kt[abs(dt)] / 50.0, rel=1e-12, abs=1e-16)
+    assert r.slack[15, 10, 10] == 0 and r.amb[15, 10, 10] == 1          # k_s(1, 0) = 0
+    assert r.slack[10, 10, 12] == 0 and r.amb[10, 10, 12] == 1          # k_t(1) = 0
+    assert (r.slack[r.amb == 0] == 0).all() and (r.slack >= 0).all()
+    assert r.slack.sum() == pytest.approx(8 * ks34 * (kt[0] + 2 * kt[1]) / 50.0, rel=1e-12, abs=1e-15)
+    i, j = np.meshgrid(np.arange(-6, 7), np.arange(-6, 7))
+    interior = int((i * i + j * j < 25).sum())
+    assert int(r.amb.sum()) == 12 * 5 + interior * 2
+
+
+def test_slack_edge_jump_bound(oracle_mod):
+    # On random inputs every ambiguous pair is within 1e-6 (relative) of an edge, so its
+    # |k_s k_t| is at most the printed kernel's edge value: spatial edge (pi/2)(1 - 1/sqrt2)^4
+    # = 0.011560 (the maximum of k_s on the unit circle, up to 1e-5 for the 1e-6
+    # band) times k_t <= 3/4; temporal edge k_t <= 3/4 (1e-6)^2.  A voxel's slack is bounded
+    # by (its ambiguous pair count) x that / (n hs^2 ht); with points on a lattice of voxel
+    # centres and integer hs, ht the ambiguous pairs of a voxel are the lattice points at
+    # exact distance hs (or exact |dt| = ht), counted here by integer geometry.
+    g = grid(G=(24, 24, 16), res=1.0, hs=5.0, ht=2.0)
+    rng = synth.SplitMix64(7)
+    n = 60
+    P = np.stack([np.floor(rng.uniform(0, 24, n)), np.floor(rng.uniform(0, 24, n)),
+                  np.floor(rng.uniform(0, 16, n))], axis=1)
+    pts = (P + 0.5).astype(np.float32)
+    r = oracle_mod.stkde_pb(pts, **g)
+    X, Y, T = np.meshgrid(np.arange(24), np.arange(24), np.arange(16), indexing="ij")
+    m = np.zeros(X.shape, np.int64)
+    for px, py, pt in P.astype(np.int64):
+        d2 = (X - px) ** 2 + (Y - py) ** 2
+        dt = np.abs(T - pt)
+        m += ((d2 == 25) & (dt <= 2)) | ((d2 <= 25) & (dt == 2))
+    edge = (math.pi / 2) * (1 - 1 / math.sqrt(2)) ** 4
+    bound = m * (edge * (1 + 1e-5) * 0.75) / (n * 25 * 2)
+    assert (r.slack <= bound + 1e-300).all()
+    assert ((m > 0) == (r.amb == 1)).all()
+    assert r.slack.max() > 0
