@@ -85,10 +85,52 @@ def peaks():
 
 
 def host_cores():
+    """Threads the oracle legs use (the cores this process may run on)."""
     try:
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+def host_cpu():
+    """{physical_cores, logical_cpus, model} of this host (lscpu's Core(s) per socket x
+    Socket(s), else /proc/cpuinfo's distinct (physical id, core id) pairs)."""
+    model, phys, logical = None, None, os.cpu_count()
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {a.strip(): b.strip() for a, b in (ln.split(":", 1) for ln in out.splitlines() if ":" in ln)}
+        model = kv.get("Model name")
+        if "Core(s) per socket" in kv and "Socket(s)" in kv:
+            phys = int(kv["Core(s) per socket"]) * int(kv["Socket(s)"])
+    except Exception:
+        pass
+    if phys is None or model is None:
+        try:
+            cores, m = set(), None
+            pid = cid = None
+            for ln in open("/proc/cpuinfo"):
+                k, _, v = ln.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name":
+                    m = m or v
+                elif k == "physical id":
+                    pid = v
+                elif k == "core id":
+                    cid = v
+                elif not k and pid is not None:
+                    cores.add((pid, cid))
+                    pid = cid = None
+            phys = phys or (len(cores) or None)
+            model = model or m
+        except Exception:
+            pass
+    return {"physical_cores": phys, "logical_cpus": logical, "model": model}
+
+
+def cpu_baseline_dict(value, sample):
+    d = {"value": value, "unit": UNIT, "cores": host_cores(), "kind": "oracle", "sample": sample}
+    d.update({"host_" + k: v for k, v in host_cpu().items()})
+    return d
 
 
 # ----------------------------------------------------------------- clocks ---
@@ -186,13 +228,12 @@ def reference_main(args, w, rank):
         vals.append(C / dt)
         secs.append(dt)
     v = statistics.median(vals)
-    cores = host_cores()
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(secs),
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic", "config": config_dict(w, None, variant_config(args.variant)),
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample}}
+           "cpu_baseline": cpu_baseline_dict(v, sample)}
     print(json.dumps(out))
     return 0
 
@@ -258,13 +299,10 @@ def gpu_main(args, w, rank, world, local_rank):
         else:
             cuts = plan.slab_partition(pts, world, stream=stream) if world > 1 else [0, w.G[2]]
         t0, t1 = cuts[0 if xsplit else rank], cuts[1 if xsplit else rank + 1]
-        if xsplit:   # the metric's C is the whole grid's: count it on rank 0 only
-            if rank != 0:
-                C = 0
-            elif variant == "adaptive":
-                C = int(plan.count_contributions_adaptive(pts, bw, 0, w.G[2], stream=stream).item())
-            else:
-                C = int(plan.count_contributions(pts, 0, w.G[2], stream=stream).item())
+        if xsplit and variant == "adaptive":   # the metric's C is the whole grid's: count it on rank 0
+            C = int(plan.count_contributions_adaptive(pts, bw, 0, w.G[2], stream=stream).item()) if rank == 0 else 0
+        elif xsplit:                           # this rank's own contributions (its x-slab), exactly
+            C = int(plan.count_contributions_box(pts, x0, x1, 0, w.G[2], stream=stream).item()) if x1 > x0 else 0
         elif t1 <= t0:
             C = 0
         elif variant == "adaptive":
@@ -280,6 +318,7 @@ def gpu_main(args, w, rank, world, local_rank):
     if world > 1:
         dist.all_reduce(Ct)
     C_total = int(Ct.item())
+    C_own = C if not (xsplit and variant == "adaptive") else None   # exact per-rank count (None: estimate)
     odt = torch.float64 if variant == "f64" else torch.float32
     out = (torch.empty((max(x1 - x0, 1), w.G[1], w.G[2]), dtype=odt, device=dev) if xsplit else
            torch.empty((w.G[0], w.G[1], max(t1 - t0, 1)), dtype=odt, device=dev))
@@ -446,7 +485,9 @@ def gpu_main(args, w, rank, world, local_rank):
     (hbm_peak, hbm_src), (bf16_peak, bf16_src) = peaks()
     grid_bytes = (x1 - x0) * w.G[1] * (t1 - t0) * esz * len(outs)
     t_hbm = grid_bytes / (hbm_peak * 1e9)
-    C_rank = C_total / world if xsplit else C       # x-slabs: per-rank work ~ C / N (cost-balanced cuts)
+    # this rank's own work (exact for the fixed variant; the adaptive x-slab count is the global
+    # one, so its per-rank share is estimated as C / N over the cost-balanced cuts)
+    C_rank = C_own if C_own is not None else C_total / world
     t_fp32 = 2.0 * C_rank / (FP32_NOMINAL_TFLOPS * 1e12)
     if variant == "f64" and 2.0 * C_rank / (FP64_NOMINAL_TFLOPS * 1e12) >= t_hbm:
         ach = 2.0 * C_rank / (kernel_ms * 1e-3) / 1e12
@@ -485,6 +526,46 @@ def gpu_main(args, w, rank, world, local_rank):
                    # tile contraction that is inside some disc and window
                    "useful_fraction": C_rank / (128 * 32 * mma_cols / args.steps)}
 
+    if world > 1:       # the line carries rank 0's roofline; the slowest rank's fraction too
+        fr_t = torch.tensor([roof["frac"]], dtype=torch.float64, device=dev)
+        dist.all_reduce(fr_t, op=dist.ReduceOp.MIN)
+        roof["rank"] = 0
+        roof["frac_min_over_ranks"] = float(fr_t.item())
+
+    # ---- optional whole-grid gather (outside the timed region, reported separately) ----
+    # x-slabs are contiguous row blocks of the [Gx][Gy][Gt] layout: rank r's slab lands in rows
+    # [cut_r, cut_r+1) of rank 0's grid by one NCCL recv per rank (point-to-point over NVLink)
+    gather = None
+    if world > 1 and xsplit and variant == "fixed":
+        full = torch.empty(tuple(w.G), dtype=torch.float32, device=dev) if rank == 0 else None
+        def do_gather():
+            ops = []
+            if rank == 0:
+                full[x0:x1].copy_(out[:x1 - x0])
+                for r in range(1, world):
+                    a, b = xcuts[r], xcuts[r + 1]
+                    if b > a:
+                        ops.append(dist.P2POp(dist.irecv, full[a:b], r))
+            elif x1 > x0:
+                ops.append(dist.P2POp(dist.isend, out[:x1 - x0].contiguous(), 0))
+            if ops:
+                for q in dist.batch_isend_irecv(ops):
+                    q.wait()
+        do_gather()                                   # warm-up (NCCL P2P connection setup)
+        barrier()
+        gb_, ge_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        gb_.record()
+        do_gather()
+        ge_.record()
+        barrier()
+        g_ms = torch.tensor([gb_.elapsed_time(ge_)], dtype=torch.float64, device=dev)
+        dist.all_reduce(g_ms, op=dist.ReduceOp.MAX)
+        gbytes = (w.G[0] - (x1 - x0 if rank == 0 else 0)) * w.G[1] * w.G[2] * 4
+        gather = {"ms": float(g_ms.item()), "bytes_to_root": gbytes,
+                  "how": "NCCL batch_isend_irecv: each rank's x-slab into its rows of rank 0's grid",
+                  "timed_in_value": False}
+        del full
+
     result = None
     if rank == 0:
         cpu = None
@@ -493,9 +574,8 @@ def gpu_main(args, w, rank, world, local_rank):
             if variant == "sweep":
                 m = max(m // len(fr), 1)
             Cs, dt = run_oracle_sample(w, m, variant)
-            cpu = {"value": Cs / dt, "unit": UNIT, "cores": host_cores(), "kind": "oracle",
-                   "sample": "first %d of %d points, full %dx%dx%d grid, FP64 oracle (PB form%s), %.1f s"
-                             % (m, w.n, *w.G, "" if variant == "fixed" else ", " + variant, dt)}
+            cpu = cpu_baseline_dict(Cs / dt, "first %d of %d points, full %dx%dx%d grid, FP64 oracle (PB form%s), %.1f s"
+                                    % (m, w.n, *w.G, "" if variant == "fixed" else ", " + variant, dt))
         result = {
             "metric": METRIC, "value": C_total / (ms_max * 1e-3), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
@@ -526,6 +606,8 @@ def gpu_main(args, w, rank, world, local_rank):
             result["variant"] = variant
         if separate_ms is not None:
             result["separate_ms"] = separate_ms
+        if gather is not None:
+            result["gather"] = gather
         print(json.dumps(result))
     plan.close()
     if world > 1:
@@ -546,6 +628,69 @@ def profile_traffic(name, engine, variant="fixed"):
     return None
 
 
+def free_port():
+    import socket
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 without a torchrun environment: start N ranks (one per GPU) under
+    torch.distributed.run on this node and pass rank 0's JSON line through."""
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(json.dumps({"n_gpus": args.gpus, "error": "--gpus %d but only %d CUDA device(s) visible"
+                              % (args.gpus, have)}))
+            return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=dict(os.environ, STKDE_BENCH_LAUNCHED="1"))
+
+
+def dry_main(args, w, rank, world):
+    """--dry-run: the N-rank control flow of the bench on CPU (gloo, no CUDA): process group,
+    cost-balanced x-slab cuts from the library's host-only partition (stkde_xslab_cuts),
+    per-rank work, barrier + max-over-ranks timing, one JSON line from rank 0.  The per-rank
+    'work' is a stand-in (its slab's point count), not the method: tests/test_bench_cpu.py."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1705_09366_b200 as S
+    if world > 1:
+        dist.init_process_group("gloo")
+    g = w.grid_kwargs()
+    X = np.clip(np.floor((w.points[:, 0].astype(np.float64) - g["x0"]) / g["sres"]).astype(np.int64), 0, w.G[0] - 1)
+    hist = np.bincount(X, minlength=w.G[0]).astype(np.int64)
+    cuts = S.xslab_cuts(w.G, w.hs / w.sres, w.ht / w.tres, hist, world)
+    x0, x1 = cuts[rank], cuts[rank + 1]
+    mine = torch.tensor([int(((X >= x0) & (X < x1)).sum())], dtype=torch.int64)
+    if world > 1:
+        dist.all_reduce(mine)
+    ms = []
+    for _ in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        _ = int(((X >= x0) & (X < x1)).sum())
+        if world > 1:
+            dist.barrier()
+        ms.append(1e3 * (time.perf_counter() - t0))
+    v = torch.tensor([statistics.mean(ms[args.warmup:])], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": float(v.item()), "backend": "gloo",
+                          "config": {"workload": w.name, "parallelism": "x-slab x%d" % world, "slab_cuts": cuts,
+                                     "points_total": int(mine.item())}}))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -555,13 +700,21 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="fixed", choices=["fixed", "adaptive", "sweep", "f64"])
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU-only: the N-rank control flow over gloo, no CUDA (tests)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and not os.environ.get("STKDE_BENCH_LAUNCHED"):
+        return self_launch(args)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and rank == 0:
-        print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
+    if world != args.gpus:
+        if rank == 0:
+            print(json.dumps({"n_gpus": args.gpus, "error": "--gpus %d but WORLD_SIZE %d" % (args.gpus, world)}))
+        return 2
     w = synth.make_config(args.config)
+    if args.dry_run:
+        return dry_main(args, w, rank, world)
     if args.impl == "reference":
         return reference_main(args, w, rank)
     return gpu_main(args, w, rank, world, local_rank)
