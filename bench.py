@@ -343,8 +343,19 @@ def gpu_main(args, w, rank, world, local_rank):
         else:
             plan.compute_slab(p_pts, t0, t1, n_norm=w.n, out=out, stream=stream)
 
+    # N = 1, fixed variant: the step is ONE CUDA-graph launch of the captured pass
+    # (stkde_graph_create: binning, work list and tile kernel, ~20 kernels) -- the small grids
+    # are launch-bound otherwise.  Same kernels, same work; --no-graph launches them one by one.
+    graph = None
+    if world == 1 and variant == "fixed" and not args.no_graph:
+        with torch.cuda.stream(stream):
+            graph = plan.graph(pts, out=out)
+
     def step():
-        run(pts, bw)
+        if graph is not None:
+            graph.launch(stream)
+        else:
+            run(pts, bw)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -375,6 +386,16 @@ def gpu_main(args, w, rank, world, local_rank):
                 e1.record(stream)
         barrier()
     ms_steps = [a.elapsed_time(b) for a, b in ev]
+    if graph is not None:
+        # the tile kernel's launch duration: the same steps launched one by one (a graph
+        # replays no per-launch event records), CUDA events on the compute stream
+        kms, klaunch = plan.kernel_ms()          # (resets nothing recorded inside the graph)
+        plan.enable_kernel_timing(True)
+        with torch.cuda.stream(stream):
+            for _ in range(args.steps):
+                flush.fill_(1)
+                run(pts, bw)
+        barrier()
     kms, klaunch = plan.kernel_ms()
     plan.enable_kernel_timing(False)
     mma_cols, mma_kblocks = plan.mma_stats()
@@ -587,6 +608,7 @@ def gpu_main(args, w, rank, world, local_rank):
                 "parallelism": ("x-slab x%d" if xsplit else "time-slab x%d") % world,
                 "slab_cuts": xcuts if xsplit else cuts,
                 "l2": "flushed between timed steps (256 MiB write, untimed)",
+                "launch": "one CUDA graph per step (stkde_graph_launch)" if graph is not None else "kernel by kernel",
                 "inputs_resident": True})),
             "e2e": {"value": C_total / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
@@ -700,6 +722,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--variant", default="fixed", choices=["fixed", "adaptive", "sweep", "f64"])
+    ap.add_argument("--no-graph", action="store_true",
+                    help="launch the pass kernel by kernel instead of one CUDA-graph launch per step")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU-only: the N-rank control flow over gloo, no CUDA (tests)")
     args = ap.parse_args()

@@ -112,6 +112,22 @@ int stkde_compute_slab(stkde_plan_t plan, const float *d_points, int64_t n,
                        int64_t n_norm, int64_t t_begin, int64_t t_end,
                        float *d_slab, void *stream);
 
+/* ---- CUDA graphs (launch-bound small grids: one launch instead of ~20) ----
+ * stkde_graph_create captures ONE stkde_compute_slab call (arguments as there; the full
+ * grid is t_begin = 0, t_end = Gt, n_norm = n) on a private stream into an instantiated
+ * CUDA graph; nothing runs at creation.  stkde_graph_launch replays it on `stream`: the
+ * whole pass (binning, work list, tile kernel) as one graph launch, reading d_points and
+ * writing d_out AS THEY ARE at launch time (the caller may refill the point buffer between
+ * launches; n, the slab and the buffers are fixed at capture).  The graph uses the plan's
+ * workspace: the plan must outlive it, and a graph must not run concurrently with another
+ * call on the same plan.  Errors: as stkde_compute_slab, STKDE_ECUDA if capture or
+ * instantiation fails, STKDE_ENOMEM. */
+typedef struct stkde_graph_s *stkde_graph_t;
+int stkde_graph_create(stkde_plan_t plan, const float *d_points, int64_t n, int64_t n_norm,
+                       int64_t t_begin, int64_t t_end, float *d_out, stkde_graph_t *out);
+int stkde_graph_launch(stkde_graph_t graph, void *stream);
+void stkde_graph_destroy(stkde_graph_t graph);
+
 /* Cost-balanced, Bt-aligned time-slab cuts for `nparts` devices (tcgen05
  * engine: when nparts exceeds ceil(Gt/Bt) the cut granularity is halved down
  * to 32 layers -- its slabs are bitwise equal to the full grid at any boundary).

@@ -154,7 +154,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     const int64_t cand_bound = std::max<int64_t>(max_n, 1) * nb;
     // split-tile partial slot: tcgen05 engine int64 exact sums per voxel, legacy engines FP32
     const size_t tile_bytes = (size_t)(p->engine == STKDE_ENGINE_TC ? 128 * 8 : 256 * 4) * BT;
-    const int64_t slot_budget = (int64_t)env_int("STKDE_SLOT_MB", 1024) * (1 << 20) / (int64_t)tile_bytes;
+    const int64_t slot_budget = (int64_t)env_int("STKDE_SLOT_MB", 4096) * (1 << 20) / (int64_t)tile_bytes;
     int64_t chunk = std::max<int64_t>(env_int("STKDE_CHUNK", 4096), (2 * cand_bound + slot_budget - 1) / slot_budget);
     // tcgen05 engine: the S32 accumulators take <= 129888 per point (D16: hl + mm + lh
     // + the ICOMP = 93 indicator), so a work item may accumulate at most
@@ -169,7 +169,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
         if (need > 16384) {
             set_error("max_n = %lld needs %lld-candidate work items for the %d MiB split-slot budget "
                       "(STKDE_SLOT_MB), above the 16384-candidate S32 limit: lower max_n or raise STKDE_SLOT_MB",
-                      (long long)max_n, (long long)need, env_int("STKDE_SLOT_MB", 1024));
+                      (long long)max_n, (long long)need, env_int("STKDE_SLOT_MB", 4096));
             free(p);
             return STKDE_EINVAL;
         }
@@ -221,6 +221,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
         {(void **)&p->bucket_cnt, ((size_t)p->nbuckets + 1) * 4}, {(void **)&p->bucket_begin, ((size_t)p->nbuckets + 2) * 4},
         {(void **)&p->lpt_key_in, nt * 4}, {(void **)&p->lpt_key_out, nt * 4},
         {(void **)&p->lpt_val_in, nt * 4}, {(void **)&p->lpt_val_out, nt * 4},
+        {(void **)&p->tile_cnt, nt * 4},
         {(void **)&p->chunk_pack, (nt + 1) * 8}, {(void **)&p->chunk_off, (nt + 1) * 8},
         {(void **)&p->items, (size_t)p->max_items * 16},
         {(void **)&p->arrive, nt * 4},
@@ -250,6 +251,8 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     p->tc_profile = env_int("STKDE_TC_PROF", 0);
     p->tc_watchdog = env_int("STKDE_TC_WATCHDOG", 0);
     p->no_tma = env_int("STKDE_NO_TMA", 0);
+    p->order = env_int("STKDE_ORDER", -1);       // -1: by the slab's tile count (launch_worklist)
+    p->heavy = env_int("STKDE_HEAVY", p->chunk / 4);
     *out = p;
     return STKDE_OK;
 }
@@ -315,12 +318,10 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
     // depend on the candidate grouping); the FP32 engines keep the full binning so a slab
     // stays bitwise equal to the full grid's layers
     const bool slab_cull = p->engine == STKDE_ENGINE_TC;
-    int rc = launch_binning(p, d_points, n, st, slab_cull ? t_begin : 0, slab_cull ? t_end : (int64_t)g.Gt);
+    // (tcgen05 engine: the chord table is written by the binning's scatter pass)
+    int rc = launch_binning(p, d_points, n, st, slab_cull ? t_begin : 0, slab_cull ? t_end : (int64_t)g.Gt,
+                            p->engine == STKDE_ENGINE_TC);
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
-    if (p->engine == STKDE_ENGINE_TC) {
-        rc = launch_chords(p, n, st);
-        if (rc) { set_error("chord launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
-    }
     const int c0 = (int)(t_begin / g.BT), c1 = (int)((t_end + g.BT - 1) / g.BT);
     rc = launch_worklist(p, c0, c1, st);
     if (rc) { set_error("work-list launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
@@ -334,6 +335,73 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
 extern "C" int stkde_compute(stkde_plan_t p, const float *d_points, int64_t n, float *d_grid, void *stream) {
     if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
     return compute_slab_impl(p, d_points, n, n, 0, p->g.Gt, d_grid, (cudaStream_t)stream);
+}
+
+// ---- CUDA graphs: one compute call captured once, replayed with a single launch ----
+struct stkde_graph_s {
+    cudaGraph_t graph;
+    cudaGraphExec_t exec;
+    int device;
+};
+
+extern "C" int stkde_graph_create(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm, int64_t t_begin,
+                                  int64_t t_end, float *d_out, stkde_graph_t *out) {
+    if (!p || !out) { set_error("NULL argument"); return STKDE_EINVAL; }
+    *out = nullptr;
+    CK(cudaSetDevice(p->device));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const int timing = p->timing;
+    p->timing = 0;                                     // no event nodes in the graph
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    int rc = STKDE_OK;
+    if (e == cudaSuccess) {
+        rc = compute_slab_impl(p, d_points, n, n_norm, t_begin, t_end, d_out, s);
+        e = cudaStreamEndCapture(s, &graph);
+    }
+    p->timing = timing;
+    cudaStreamDestroy(s);
+    if (rc != STKDE_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return rc;
+    }
+    if (e != cudaSuccess) {
+        set_error("graph capture failed: %s", cudaGetErrorString(e));
+        if (graph) cudaGraphDestroy(graph);
+        return STKDE_ECUDA;
+    }
+    stkde_graph_s *g = (stkde_graph_s *)calloc(1, sizeof(stkde_graph_s));
+    if (!g) { cudaGraphDestroy(graph); set_error("host allocation failed"); return STKDE_ENOMEM; }
+    g->graph = graph;
+    g->device = p->device;
+    e = cudaGraphInstantiate(&g->exec, graph, 0);
+    if (e != cudaSuccess) {
+        set_error("graph instantiation failed: %s", cudaGetErrorString(e));
+        cudaGraphDestroy(graph);
+        free(g);
+        return STKDE_ECUDA;
+    }
+    *out = g;
+    return STKDE_OK;
+}
+
+extern "C" int stkde_graph_launch(stkde_graph_t g, void *stream) {
+    if (!g) { set_error("graph is NULL"); return STKDE_EINVAL; }
+    CK(cudaSetDevice(g->device));
+    CK(cudaGraphLaunch(g->exec, (cudaStream_t)stream));
+    return STKDE_OK;
+}
+
+extern "C" void stkde_graph_destroy(stkde_graph_t g) {
+    if (!g) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(g->device);
+    cudaGraphExecDestroy(g->exec);
+    cudaGraphDestroy(g->graph);
+    cudaSetDevice(cur);
+    free(g);
 }
 
 extern "C" int stkde_compute_slab(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm, int64_t t_begin,
@@ -400,7 +468,7 @@ static int compute_f64_impl(stkde_plan_s *p, const float *d_points, const float 
         return STKDE_OK;
     }
     BwScope scope(p, d_bw);
-    int rc = launch_binning(p, d_points, n, st, t_begin, t_end);
+    int rc = launch_binning(p, d_points, n, st, t_begin, t_end, false, true);
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     // Alg. 1 divides the sum by n hs^2 ht; adaptive: terms carry 1/(hs_i^2 ht_i), the sum 1/n
     const double den = d_bw ? (double)n_norm : (double)n_norm * (g.hs * g.hs) * g.ht;

@@ -68,7 +68,7 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
                        uint32_t *__restrict__ keys, uint32_t *__restrict__ vals,
                        uint32_t *__restrict__ bucket_cnt, int *__restrict__ err, uint32_t sentinel,
                        const float *__restrict__ bw, PointBw *__restrict__ bw_rec, unsigned *__restrict__ wmax,
-                       int t_begin, int t_end) {
+                       int t_begin, int t_end, int ranks) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     float x = pts[3 * i], y = pts[3 * i + 1], t = pts[3 * i + 2];
@@ -98,10 +98,11 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
     }
     // (unbinned points keep the sentinel key and sort last; they are not counted: with slab
     // culling most points of a slab call are unbinned, and one shared counter serialised them)
-    if (key != sentinel) atomicAdd(&bucket_cnt[key], 1u);
+    // rank = this point's slot in its bucket (counting-sort path of the tcgen05 engine)
+    const uint32_t rank = key != sentinel ? atomicAdd(&bucket_cnt[key], 1u) : 0u;
     rec[i] = r;
     keys[i] = key;
-    vals[i] = (uint32_t)i;
+    vals[i] = ranks ? rank : (uint32_t)i;
 }
 
 // K1b: records (and adaptive bandwidths) in bucket order (coalesced candidate reads
@@ -176,6 +177,41 @@ __global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams
     }
 }
 
+// K1c (tcgen05 engine): counting-sort scatter.  Record i goes to bucket_begin[key] + rank,
+// its slot from k_prep's atomic bucket count: buckets are contiguous runs as with the radix
+// sort, but the order inside a bucket is the atomics' order.  The tcgen05 tile sums are exact
+// integers, independent of the candidates' order and grouping, and every voxel is rounded
+// once from its sum, so the grid is bitwise the same for any order.  With
+// chords != NULL, thread (i, blk) also writes the point's chord block blk at the sorted
+// position (the k_chords table, fused: one pass over the records).
+__global__ void k_scatter(const PointRec *__restrict__ rec, const uint32_t *__restrict__ keys,
+                          const uint32_t *__restrict__ ranks, const uint32_t *__restrict__ bucket_begin,
+                          uint32_t sentinel, int64_t n, PointRec *__restrict__ out, const PointBw *__restrict__ bw_rec,
+                          PointBw *__restrict__ bw_out, GridParams gp, uint16_t *__restrict__ chords, int nb) {
+    const int64_t total = n * nb;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = e / nb;
+        const int blk = (int)(e - i * nb);
+        const uint32_t key = keys[i];
+        if (key == sentinel) continue;
+        const int64_t j = (int64_t)bucket_begin[key] + ranks[i];
+        const PointRec r = rec[i];
+        if (blk == 0) {
+            out[j] = r;
+            if (bw_rec) bw_out[j] = bw_rec[i];
+        }
+        if (chords) {
+            const GridParams g = bw_rec ? with_point_bw(gp, bw_rec[i]) : gp;
+            const int Y0 = ((r.Y - g.Hs) & ~7) + 8 * blk;
+            uint32_t w[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                w[k] = chord_entry(g, r, Y0 + 2 * k) | (chord_entry(g, r, Y0 + 2 * k + 1) << 16);
+            reinterpret_cast<uint4 *>(chords)[j * nb + blk] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+    }
+}
+
 // Candidate count of a tile: sum of its home-bucket segments.
 __device__ __forceinline__ uint32_t tile_candidates(const GridParams &g, const uint32_t *__restrict__ bb,
                                                     int a, int b, int c) {
@@ -192,23 +228,34 @@ __device__ __forceinline__ uint32_t tile_candidates(const GridParams &g, const u
     return s;
 }
 
-// K3a: per slab tile, candidate count -> LPT key (descending count).
+// K3a: per slab tile, candidate count and work-list sort key (stable radix sort, ascending).
+//   order 0 (LPT, "most loaded subdomain first"): descending count;
+//   order 1 (locality): tiles with >= `heavy` candidates first by descending count, then the
+//     rest in slab-tile order (x fastest, then y, then the layer block), so the persistent
+//     CTAs work on neighbouring tiles at the same time and their candidate records and
+//     chords are shared in L2 instead of re-read from DRAM.
+// Counts are clamped to 16 bits in the key (the order only needs to be approximate; the
+// exact count is kept in tcnt for the chunking).
 __global__ void k_tile_counts(GridParams g, const uint32_t *__restrict__ bucket_begin, int c0, int nsl,
-                              uint32_t *__restrict__ lkey, uint32_t *__restrict__ lval) {
+                              uint32_t *__restrict__ lkey, uint32_t *__restrict__ lval, uint32_t *__restrict__ tcnt,
+                              int order, uint32_t heavy) {
     int ls = blockIdx.x * blockDim.x + threadIdx.x;
     if (ls >= nsl) return;
     int a = ls % g.NXA + g.XA0, b = (ls / g.NXA) % g.NTY, c = ls / (g.NXA * g.NTY) + c0;
     uint32_t cnt = tile_candidates(g, bucket_begin, a, b, c);
-    lkey[ls] = 0xFFFFFFFFu - cnt;
+    const uint32_t lpt = 0xFFFFu - min(cnt, 0xFFFFu);
+    lkey[ls] = (order == 0 || cnt >= heavy) ? lpt : 0x10000u + (uint32_t)ls;
     lval[ls] = (uint32_t)ls;
+    tcnt[ls] = cnt;
 }
 
-// K3b: chunks per tile (in LPT order) packed with split-slot demand.
-__global__ void k_chunk_pack(const uint32_t *__restrict__ lkey, int nsl, int chunk, uint64_t *__restrict__ pack) {
+// K3b: chunks per tile (in work-list order) packed with split-slot demand.
+__global__ void k_chunk_pack(const uint32_t *__restrict__ lval, const uint32_t *__restrict__ tcnt, int nsl, int chunk,
+                             uint64_t *__restrict__ pack) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k > nsl) return;
     if (k == nsl) { pack[k] = 0; return; }
-    uint32_t cnt = 0xFFFFFFFFu - lkey[k];
+    uint32_t cnt = tcnt[lval[k]];
     uint32_t nch = cnt == 0 ? 1u : (cnt + chunk - 1) / chunk;
     uint64_t slots = nch > 1 ? nch : 0;
     pack[k] = (uint64_t)nch | (slots << 32);
@@ -305,28 +352,45 @@ __global__ void k_gather(const float *__restrict__ slab, int64_t rows, int64_t G
 static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
 int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st, int64_t t_begin,
-                   int64_t t_end) {
+                   int64_t t_end, bool with_chords, bool stable) {
     const GridParams &g = p->g;
     cudaMemsetAsync(p->bucket_cnt, 0, (p->nbuckets + 1) * sizeof(uint32_t), st);
     const bool ad = p->d_bw != nullptr;
+    // tcgen05 engine: counting-sort scatter by the atomic bucket ranks (order-free exact sums);
+    // the FP32 engines keep the stable radix sort (their sums depend on the order)
+    // (stable: the FP64-output path sums each voxel in bucket-then-input order)
+    const bool counting = p->engine == STKDE_ENGINE_TC && !stable;
     if (ad) cudaMemsetAsync(p->counters + 6, 0, sizeof(int), st);
     k_prep<<<nblk(n, 256), 256, 0, st>>>(d_points, n, g, p->rec, p->keys_in, p->vals_in, p->bucket_cnt,
                                           p->counters + 1, (uint32_t)p->nbuckets, p->d_bw,
                                           ad ? p->bw_rec : nullptr, reinterpret_cast<unsigned *>(p->counters + 6),
-                                          (int)t_begin, (int)t_end);
+                                          (int)t_begin, (int)t_end, counting ? 1 : 0);
     size_t bytes = p->cub_bytes;
-    if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->keys_in, p->keys_out, p->vals_in, p->vals_out,
-                                        (int)n, 0, p->key_bits, st) != cudaSuccess)
-        return STKDE_ECUDA;
-    bytes = p->cub_bytes;
+    if (!counting) {
+        if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->keys_in, p->keys_out, p->vals_in, p->vals_out,
+                                            (int)n, 0, p->key_bits, st) != cudaSuccess)
+            return STKDE_ECUDA;
+        bytes = p->cub_bytes;
+    }
     if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->bucket_cnt, p->bucket_begin, (int)(p->nbuckets + 1), st) !=
         cudaSuccess)
         return STKDE_ECUDA;
-    // bucket_begin[nbuckets] = the number of binned points (the sentinel bucket sorts last)
-    k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n, ad ? p->bw_rec : nullptr,
-                                             p->bw_sorted, p->bucket_begin + p->nbuckets);
-    p->last_own_launches += 2;
-    p->last_cub_calls += 2;
+    if (counting) {
+        // bucket_begin[nbuckets] = the number of binned points
+        const int nb = with_chords ? chord_rows(g.Hs) / 8 : 1;
+        const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n * nb + 255) / 256, (int64_t)p->num_sms * 32));
+        k_scatter<<<blocks, 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin, (uint32_t)p->nbuckets, n,
+                                          p->rec_sorted, ad ? p->bw_rec : nullptr, p->bw_sorted, g,
+                                          with_chords ? p->chords : nullptr, nb);
+        p->last_own_launches += 2;
+        p->last_cub_calls += 1;
+    } else {
+        // bucket_begin[nbuckets] = the number of binned points (the sentinel bucket sorts last)
+        k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n, ad ? p->bw_rec : nullptr,
+                                                 p->bw_sorted, p->bucket_begin + p->nbuckets);
+        p->last_own_launches += 2;
+        p->last_cub_calls += 2;
+    }
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }
 
@@ -344,12 +408,18 @@ int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
     const GridParams &g = p->g;
     int nsl = g.NXA * g.NTY * (c1 - c0);
-    k_tile_counts<<<nblk(nsl, 256), 256, 0, st>>>(g, p->bucket_begin, c0, nsl, p->lpt_key_in, p->lpt_val_in);
+    // locality order only for grids with many tiles per SM (few tiles: LPT balances the SMs)
+    const int order = p->order >= 0 ? p->order : (nsl >= 64 * p->num_sms ? 1 : 0);
+    k_tile_counts<<<nblk(nsl, 256), 256, 0, st>>>(g, p->bucket_begin, c0, nsl, p->lpt_key_in, p->lpt_val_in,
+                                                  p->tile_cnt, order, (uint32_t)p->heavy);
+    int kbits = 16;                                  // LPT keys < 2^16; locality keys < 2^16 + nsl
+    if (order != 0)
+        while (kbits < 31 && (int64_t(1) << kbits) < 0x10000 + (int64_t)nsl) ++kbits;
     size_t bytes = p->cub_bytes;
     if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->lpt_key_in, p->lpt_key_out, p->lpt_val_in,
-                                        p->lpt_val_out, nsl, 0, 32, st) != cudaSuccess)
+                                        p->lpt_val_out, nsl, 0, kbits, st) != cudaSuccess)
         return STKDE_ECUDA;
-    k_chunk_pack<<<nblk(nsl + 1, 256), 256, 0, st>>>(p->lpt_key_out, nsl, p->chunk, p->chunk_pack);
+    k_chunk_pack<<<nblk(nsl + 1, 256), 256, 0, st>>>(p->lpt_val_out, p->tile_cnt, nsl, p->chunk, p->chunk_pack);
     bytes = p->cub_bytes;
     if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->chunk_pack, p->chunk_off, nsl + 1, st) != cudaSuccess)
         return STKDE_ECUDA;

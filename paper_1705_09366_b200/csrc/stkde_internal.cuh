@@ -200,6 +200,9 @@ struct stkde_plan_s {
     uint32_t *bucket_cnt;       // [ntiles + 1]
     uint32_t *bucket_begin;     // [ntiles + 2]
     uint32_t *lpt_key_in, *lpt_key_out, *lpt_val_in, *lpt_val_out;   // [ntiles]
+    uint32_t *tile_cnt;         // [ntiles] candidate count per slab tile
+    int order;                  // work-list order: 0 = LPT, 1 = heavy tiles by LPT, then locality, -1 = by size
+    int heavy;                  // candidates from which a tile counts as heavy (order 1)
     uint64_t *chunk_pack, *chunk_off;   // [ntiles + 1]
     int4 *items;                // [max_items]
     uint32_t *arrive;           // [ntiles]
@@ -229,8 +232,10 @@ struct stkde_plan_s {
 namespace stkde {
 // launchers (stkde_binning.cu / stkde_tile.cu)
 // bins the points whose window reaches layers [t_begin, t_end) (the slab being computed)
+// (tcgen05 engine: counting-sort scatter unless `stable` (radix sort: each bucket in input
+// order); with_chords also writes the chord table in the same pass)
 int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st, int64_t t_begin,
-                   int64_t t_end);
+                   int64_t t_end, bool with_chords = false, bool stable = false);
 int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st);
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,

@@ -26,7 +26,7 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
            "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_check_flags", "stkde_count_contributions_box",
-           "stkde_strerror",
+           "stkde_graph_create", "stkde_graph_launch", "stkde_graph_destroy", "stkde_strerror",
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
            "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
            "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x",
@@ -79,6 +79,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_mma_stats.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
     L.stkde_plan_check_flags.argtypes = [P, ctypes.POINTER(ctypes.c_uint32)]
     L.stkde_count_contributions_box.argtypes = [P, P, I64, I64, I64, I64, I64, P, P]
+    L.stkde_graph_create.argtypes = [P, P, I64, I64, I64, I64, P, ctypes.POINTER(P)]
+    L.stkde_graph_launch.argtypes = [P, P]
+    L.stkde_graph_destroy.argtypes = [P]
+    L.stkde_graph_destroy.restype = None
     # development diagnostics: exported only by a -DSTKDE_TC_DIAG=1 build (csrc/stkde_diag.h)
     DIAG = ("stkde_plan_tc_profile", "stkde_plan_debug_progress")
     if hasattr(L, DIAG[0]):
@@ -105,7 +109,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
                  "stkde_plan_mma_stats", "stkde_plan_check_flags", "stkde_count_contributions_box",
-                 "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
+                 "stkde_graph_create", "stkde_graph_launch", "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
                  "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts",
                  "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x", "stkde_compute_f64",
                  "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64") + (DIAG if hasattr(L, DIAG[0]) else ()):
@@ -209,6 +213,23 @@ class Plan:
         _check(load_library().stkde_compute_slab(self._h, pts.data_ptr(), pts.shape[0], nn, int(t_begin),
                                                  int(t_end), out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
+
+    def graph(self, points: torch.Tensor, out: Optional[torch.Tensor] = None, t_begin: int = 0,
+              t_end: Optional[int] = None, n_norm: Optional[int] = None) -> "Graph":
+        """Capture one compute_slab call (default: the full grid) as a CUDA graph (stkde_graph_create):
+        Graph.launch() replays the whole pass with one launch, reading `points` and writing `out`
+        as they are at launch time."""
+        pts = _points_arg(points, self.device)
+        t1 = self.G[2] if t_end is None else int(t_end)
+        ts = t1 - int(t_begin)
+        if out is None:
+            out = torch.empty((self.G[0], self.G[1], max(ts, 0)), dtype=torch.float32, device=self.device)
+        self._check_out(out, ts)
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        h = ctypes.c_void_p()
+        _check(load_library().stkde_graph_create(self._h, pts.data_ptr(), pts.shape[0], nn, int(t_begin), t1,
+                                                 out.data_ptr(), ctypes.byref(h)))
+        return Graph(h, self, pts, out)
 
     # -- adaptive bandwidth (include/stkde.h; DESIGN.md reading R15) --
     def compute_adaptive(self, points: torch.Tensor, bw: torch.Tensor, out: Optional[torch.Tensor] = None,
@@ -405,6 +426,28 @@ class Plan:
         c, k = ctypes.c_int64(0), ctypes.c_int64(0)
         _check(load_library().stkde_plan_mma_stats(self._h, ctypes.byref(c), ctypes.byref(k)))
         return c.value, k.value
+
+
+class Graph:
+    """A captured compute call (stkde_graph_*); keeps its plan and buffers alive."""
+
+    def __init__(self, h, plan, points, out):
+        self._h, self.plan, self.points, self.out = h, plan, points, out
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+        _check(load_library().stkde_graph_launch(self._h, _stream_ptr(stream, self.plan.device)))
+        return self.out
+
+    def close(self):
+        if self._h:
+            load_library().stkde_graph_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs: Sequence[torch.Tensor],

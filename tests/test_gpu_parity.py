@@ -382,3 +382,35 @@ def test_classical_bt128_slabs(S, oracle_mod, case):
         p.check()
     ref = oracle_mod.stkde_pb(pts, kernel=kid, **g)
     assert_parity(full, ref.vol, ref.slack, ref.amb, what=name)
+
+
+@pytest.mark.parametrize("name", ["tiny", "dengue"])
+def test_graph_capture_replays_compute(S, name):
+    # the compute call is CUDA-graph capturable (include/stkde.h): a captured pass replays
+    # bitwise equal to a direct call, reads the point buffer as it is at launch time (refilled
+    # in place with another point set), and a captured slab equals the direct slab
+    w = synth.make_config(name)
+    g = w.grid_kwargs()
+    dev = torch.device("cuda", 0)
+    other = synth.uniform_points(w.n, (g["Gx"] * g["sres"], g["Gy"] * g["sres"], g["Gt"] * g["tres"]), 99)
+    with S.Plan(max_n=w.n, device=0, **g) as p:
+        t = torch.from_numpy(w.points).to(dev)
+        direct = p.compute(t).clone()
+        gr = p.graph(t)
+        for _ in range(3):
+            out = gr.launch()
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct)
+        t.copy_(torch.from_numpy(other).to(dev))          # refill in place: the graph reads it
+        out = gr.launch().clone()
+        direct2 = p.compute(t).clone()
+        torch.cuda.synchronize()
+        assert torch.equal(out, direct2) and not torch.equal(direct2, direct)
+        t0, t1 = 3, g["Gt"] - 5
+        gs = p.graph(t, t_begin=t0, t_end=t1, n_norm=w.n)
+        s = gs.launch().clone()
+        torch.cuda.synchronize()
+        assert torch.equal(s, direct2[:, :, t0:t1])
+        gr.close()
+        gs.close()
+        p.check()
