@@ -152,6 +152,12 @@ class ClockSampler:
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the first sample before the timed region starts (short regions then still have
+            # one sample on each side: the samples bracket the region)
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 2.0:
+                time.sleep(0.01)
+            self.n0 = len(self.lines)
         except Exception:
             self.proc = None
         return self
@@ -162,6 +168,9 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            n1, t0 = len(self.lines), time.time()
+            while len(self.lines) <= n1 and time.time() - t0 < 2.0:   # one sample after the region
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)

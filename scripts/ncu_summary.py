@@ -39,10 +39,14 @@ tot = sum(v for k, v in st.items() if k not in ("selected",)) or 1.0
 if st:
     s_all = sum(st.values()) or 1.0
     d["stall_share_pct"] = {k: round(100 * v / s_all, 1) for k, v in sorted(st.items(), key=lambda x: -x[1])[:10]}
+def _bytes(v):
+    num, unit = v.split()[0].replace(",", ""), (v.split() + [""])[1]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
+    return float(num) * scale
+
+
 try:
-    rb = float(d["dram__bytes_read.sum"].split()[0]) * (1e9 if "Gbyte" in d["dram__bytes_read.sum"] else 1e6)
-    wb = float(d["dram__bytes_write.sum"].split()[0]) * (1e9 if "Gbyte" in d["dram__bytes_write.sum"] else 1e6)
-    d["dram_bytes_total"] = int(rb + wb)
+    d["dram_bytes_total"] = int(_bytes(d["dram__bytes_read.sum"]) + _bytes(d["dram__bytes_write.sum"]))
 except Exception:
     pass
 d["_kernel"] = note
