@@ -197,7 +197,12 @@ __global__ void k_scatter(const PointRec *__restrict__ rec, const uint32_t *__re
         const int64_t j = (int64_t)bucket_begin[key] + ranks[i];
         const PointRec r = rec[i];
         if (blk == 0) {
-            out[j] = r;
+            // with the chord table built here, the tile kernel needs neither x nor y of the
+            // sorted record (the FP64 gates are in the chords): x carries the record's own
+            // sorted index, so the loader finds a candidate's chord row without a search
+            PointRec rs = r;
+            if (chords) rs.x = __int_as_float((int)j);
+            out[j] = rs;
             if (bw_rec) bw_out[j] = bw_rec[i];
         }
         if (chords) {
@@ -382,9 +387,11 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
         k_scatter<<<blocks, 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin, (uint32_t)p->nbuckets, n,
                                           p->rec_sorted, ad ? p->bw_rec : nullptr, p->bw_sorted, g,
                                           with_chords ? p->chords : nullptr, nb);
+        p->ridx_in_rec = with_chords ? 1 : 0;
         p->last_own_launches += 2;
         p->last_cub_calls += 1;
     } else {
+        p->ridx_in_rec = 0;
         // bucket_begin[nbuckets] = the number of binned points (the sentinel bucket sorts last)
         k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n, ad ? p->bw_rec : nullptr,
                                                  p->bw_sorted, p->bucket_begin + p->nbuckets);

@@ -194,6 +194,7 @@ struct stkde_plan_s {
     size_t ws_bytes;
     stkde::PointRec *rec, *rec_sorted;
     uint16_t *chords;           // tcgen05 engine: [max_n][chord_rows(Hs)] exact disc chords (int8 lo, hi - X_i)
+    int ridx_in_rec;            // rec_sorted[j].x holds j (the fused scatter + chord pass), else world x
     stkde::PointBw *bw_rec, *bw_sorted;   // tcgen05 engine: per-point bandwidths of an adaptive call
     const float *d_bw;          // the current call's per-point bandwidths [n][2] (NULL: fixed bandwidth)
     uint32_t *keys_in, *keys_out, *vals_in, *vals_out;
