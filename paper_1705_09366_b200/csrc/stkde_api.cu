@@ -552,12 +552,20 @@ extern "C" int stkde_compute_sweep(stkde_plan_t p, const float *d_points, int64_
     }
     int rc = launch_binning(p, d_points, n, st, 0, g0.Gt);   // once, at the plan's (largest) reach
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    // tcgen05 engine: the sorted points' world coordinates go to a side buffer (the per-point
+    // bandwidth buffer, unused by a fixed-bandwidth sweep) so each bandwidth's chord pass can
+    // read them while the records' x carries the sorted index for the loader
+    float2 *xy = p->engine == STKDE_ENGINE_TC ? reinterpret_cast<float2 *>(p->bw_rec) : nullptr;
+    if (xy && (rc = launch_save_xy(p, n, xy, st))) {
+        set_error("sweep launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+        return rc;
+    }
     const double kc = p->kernel == STKDE_KERNEL_PRINTED ? M_PI / 2.0 : 2.0 / M_PI;
     const int c0 = 0, c1 = g0.NTT;
     for (int k = 0; k < nbw; ++k) {
         p->g = narrowed(g0, h_hs[k], h_ht[k]);
         const float cnorm = (float)(kc / ((double)n * (h_hs[k] * h_hs[k]) * h_ht[k]));
-        if (p->engine == STKDE_ENGINE_TC) rc = launch_chords(p, n, st);
+        if (p->engine == STKDE_ENGINE_TC) rc = launch_chords(p, n, st, xy);
         if (!rc) rc = launch_worklist(p, c0, c1, st);
         if (!rc)
             rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)

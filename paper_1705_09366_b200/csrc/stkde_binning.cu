@@ -159,14 +159,23 @@ __device__ __forceinline__ uint32_t chord_entry(const GridParams &g, const Point
     return (uint32_t)((uint8_t)(int8_t)dl) | ((uint32_t)(uint8_t)(int8_t)dh << 8);
 }
 
-__global__ void k_chords(const PointRec *__restrict__ rec, int64_t n, GridParams gp, uint16_t *__restrict__ chords,
-                         const PointBw *__restrict__ bw, const uint32_t *__restrict__ nbinned) {
+// (the sweep: xy != NULL holds the sorted points' world coordinates, and the record's x field
+// is set to its own sorted index for the tile kernel's loader, as in k_scatter)
+__global__ void k_chords(PointRec *__restrict__ rec, int64_t n, GridParams gp, uint16_t *__restrict__ chords,
+                         const PointBw *__restrict__ bw, const uint32_t *__restrict__ nbinned,
+                         const float2 *__restrict__ xy) {
     const int nb = chord_rows(gp.Hs) / 8;            // 8-row blocks per point
     const int64_t total = min(n, (int64_t)*nbinned) * nb;   // binned points only (they sort first)
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / nb;
         const int blk = (int)(e - i * nb);
-        const PointRec r = rec[i];
+        PointRec r = rec[i];
+        if (xy) {
+            const float2 c = xy[i];
+            r.x = c.x;
+            r.y = c.y;
+            if (blk == 0) rec[i].x = __int_as_float((int)i);
+        }
         const GridParams g = bw ? with_point_bw(gp, bw[i]) : gp;
         const int Y0 = ((r.Y - g.Hs) & ~7) + 8 * blk;
         uint32_t w[4];
@@ -401,12 +410,27 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }
 
-int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st) {
+__global__ void k_save_xy(const PointRec *__restrict__ rec, int64_t n, const uint32_t *__restrict__ nbinned,
+                          float2 *__restrict__ xy) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n && j < (int64_t)*nbinned) xy[j] = make_float2(rec[j].x, rec[j].y);
+}
+
+int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st, const float2 *xy) {
     const int64_t total = n * (chord_rows(p->g.Hs) / 8);
     if (total > 0) {
         const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 32);
         k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr,
-                                         p->bucket_begin + p->nbuckets);
+                                         p->bucket_begin + p->nbuckets, xy);
+        p->last_own_launches += 1;
+    }
+    p->ridx_in_rec = xy ? 1 : 0;
+    return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
+}
+
+int launch_save_xy(stkde_plan_s *p, int64_t n, float2 *xy, cudaStream_t st) {
+    if (n > 0) {
+        k_save_xy<<<nblk(n, 256), 256, 0, st>>>(p->rec_sorted, n, p->bucket_begin + p->nbuckets, xy);
         p->last_own_launches += 1;
     }
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;

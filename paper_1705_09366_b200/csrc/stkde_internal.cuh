@@ -237,7 +237,9 @@ namespace stkde {
 // order); with_chords also writes the chord table in the same pass)
 int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st, int64_t t_begin,
                    int64_t t_end, bool with_chords = false, bool stable = false);
-int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st);
+// (xy != NULL: the sweep's saved world coordinates; the records' x then carries the sorted index)
+int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st, const float2 *xy = nullptr);
+int launch_save_xy(stkde_plan_s *p, int64_t n, float2 *xy, cudaStream_t st);
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,
                 float *out, cudaStream_t st);
