@@ -126,37 +126,65 @@ __global__ void k_permute(const PointRec *__restrict__ rec, const uint32_t *__re
 // (1, 0) for an empty row; computed once per point instead of once per
 // (point, tile) visit.  Requires H_s <= 120.  Adaptive calls (bw != NULL): the
 // disc of point i has its own radius hs_i (the table layout keeps the plan's H_s).
-// One thread per (point, aligned 8-row block): the record is read once for 8 independent
-// rows and the block is one 16-byte store.
-__device__ __forceinline__ uint32_t chord_entry(const GridParams &g, const PointRec &r, int Y) {
-    int dl = 1, dh = 0;
-    if (Y >= r.Y - g.Hs && Y <= r.Y + g.Hs) {
-        // FP32 fast path in voxel-local coordinates: column X_i + k is inside iff
-        // (k - pc)^2 + dy^2 < r^2 with pc = fx - 0.5; it is exact unless a decision
-        // falls within the FP64 band (then row_chord re-decides with Alg. 1's FP64 gate)
-        const float dyv = (float)(Y - r.Y) + 0.5f - r.fy;
-        const float dy2 = __fmul_rn(dyv, dyv);
-        const float lo_b = g.rs2 * (1.0f - GATE_BAND), hi_b = g.rs2 * (1.0f + GATE_BAND);
-        bool exact = false;
-        if (dy2 > hi_b) {
-            exact = true;                                  // empty row
-        } else if (dy2 < lo_b) {
-            const float pc = r.fx - 0.5f;
-            const float c = sqrtf(g.rs2 - dy2);
-            const int a = (int)floorf(pc - c) + 1, b = (int)ceilf(pc + c) - 1;
-            auto d2 = [&](int k) { const float dx = (float)k - pc; return __fadd_rn(__fmul_rn(dx, dx), dy2); };
-            if (a <= b && d2(a) < lo_b && d2(b) < lo_b && d2(a - 1) > hi_b && d2(b + 1) > hi_b) {
-                dl = a; dh = b;
-                exact = true;
-            }
-        }
-        if (!exact) {
-            int lo, hi;
-            row_chord(g, r, Y, &lo, &hi);
-            if (lo <= hi) { dl = lo - r.X; dh = hi - r.X; }
-        }
-    }
+// One thread per point: its 8-row blocks are 16-byte stores of one contiguous table row.
+__device__ __forceinline__ uint32_t chord_pack(int dl, int dh) {
     return (uint32_t)((uint8_t)(int8_t)dl) | ((uint32_t)(uint8_t)(int8_t)dh << 8);
+}
+// FP32 fast path in voxel-local coordinates: column X_i + k is inside iff (k - pc)^2 + dy^2 < r^2
+// with pc = fx - 0.5.  The chord ends come from an approximate sqrt (rsqrt) and are then
+// verified: both ends inside and both outer neighbours outside, each decided outside the FP64
+// band.  Returns false when a decision falls within the band (or the estimate was off by a
+// column): the caller then takes chord_entry_exact.
+__device__ __forceinline__ bool chord_entry_fast(const GridParams &g, const PointRec &r, int Y, uint32_t &e) {
+    e = chord_pack(1, 0);                                   // empty row
+    const int dyi = Y - r.Y;
+    if (dyi < -g.Hs || dyi > g.Hs) return true;
+    const float dyv = (float)dyi + 0.5f - r.fy;
+    const float dy2 = __fmul_rn(dyv, dyv);
+    const float lo_b = g.rs2 * (1.0f - GATE_BAND), hi_b = g.rs2 * (1.0f + GATE_BAND);
+    if (dy2 > hi_b) return true;
+    if (!(dy2 < lo_b)) return false;
+    const float pc = r.fx - 0.5f;
+    const float c2 = g.rs2 - dy2;
+    const float c = c2 * rsqrtf(c2);
+    const int a = __float2int_rd(pc - c) + 1, b = __float2int_ru(pc + c) - 1;
+    auto d2 = [&](int k) { const float dx = (float)k - pc; return __fadd_rn(__fmul_rn(dx, dx), dy2); };
+    if (a <= b && d2(a) < lo_b && d2(b) < lo_b && d2(a - 1) > hi_b && d2(b + 1) > hi_b) {
+        e = chord_pack(a, b);
+        return true;
+    }
+    return false;
+}
+// exact chord (row_chord: Alg. 1's FP64 gate near the edge)
+__device__ __forceinline__ uint32_t chord_entry_exact(const GridParams &g, const PointRec &r, int Y) {
+    int lo, hi;
+    row_chord(g, r, Y, &lo, &hi);
+    return lo <= hi ? chord_pack(lo - r.X, hi - r.X) : chord_pack(1, 0);
+}
+// one 8-row block of a point's chord table: block rows Y0 .. Y0 + 7 -> 4 words; the rare
+// rows the fast path cannot decide take the exact path in one (not unrolled) loop
+__device__ __forceinline__ uint4 chord_block(const GridParams &g, const PointRec &r, int Y0) {
+    uint32_t w[4];
+    unsigned need = 0u;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint32_t e0, e1;
+        if (!chord_entry_fast(g, r, Y0 + 2 * k, e0)) need |= 1u << (2 * k);
+        if (!chord_entry_fast(g, r, Y0 + 2 * k + 1, e1)) need |= 2u << (2 * k);
+        w[k] = e0 | (e1 << 16);
+    }
+#pragma unroll 1
+    while (need) {
+        const int k = __ffs(need) - 1;
+        need &= need - 1u;
+        const uint32_t v = chord_entry_exact(g, r, Y0 + k);
+        const int sh = 16 * (k & 1), wi = k >> 1;
+        const uint32_t m = ~(0xFFFFu << sh);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (q == wi) w[q] = (w[q] & m) | (v << sh);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 // (the sweep: xy != NULL holds the sorted points' world coordinates, and the record's x field
@@ -165,24 +193,19 @@ __global__ void k_chords(PointRec *__restrict__ rec, int64_t n, GridParams gp, u
                          const PointBw *__restrict__ bw, const uint32_t *__restrict__ nbinned,
                          const float2 *__restrict__ xy) {
     const int nb = chord_rows(gp.Hs) / 8;            // 8-row blocks per point
-    const int64_t total = min(n, (int64_t)*nbinned) * nb;   // binned points only (they sort first)
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / nb;
-        const int blk = (int)(e - i * nb);
+    const int64_t total = min(n, (int64_t)*nbinned);  // binned points only (they sort first)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         PointRec r = rec[i];
         if (xy) {
             const float2 c = xy[i];
             r.x = c.x;
             r.y = c.y;
-            if (blk == 0) rec[i].x = __int_as_float((int)i);
+            rec[i].x = __int_as_float((int)i);
         }
         const GridParams g = bw ? with_point_bw(gp, bw[i]) : gp;
-        const int Y0 = ((r.Y - g.Hs) & ~7) + 8 * blk;
-        uint32_t w[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-            w[k] = chord_entry(g, r, Y0 + 2 * k) | (chord_entry(g, r, Y0 + 2 * k + 1) << 16);
-        reinterpret_cast<uint4 *>(chords)[e] = make_uint4(w[0], w[1], w[2], w[3]);
+        const int Y0 = (r.Y - g.Hs) & ~7;
+        uint4 *dst = reinterpret_cast<uint4 *>(chords) + i * nb;
+        for (int blk = 0; blk < nb; ++blk) dst[blk] = chord_block(g, r, Y0 + 8 * blk);
     }
 }
 
@@ -197,31 +220,24 @@ __global__ void k_scatter(const PointRec *__restrict__ rec, const uint32_t *__re
                           const uint32_t *__restrict__ ranks, const uint32_t *__restrict__ bucket_begin,
                           uint32_t sentinel, int64_t n, PointRec *__restrict__ out, const PointBw *__restrict__ bw_rec,
                           PointBw *__restrict__ bw_out, GridParams gp, uint16_t *__restrict__ chords, int nb) {
-    const int64_t total = n * nb;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t i = e / nb;
-        const int blk = (int)(e - i * nb);
+    // one thread per point (a 64-bit e / nb per (point, block) item cost more than the chords)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t key = keys[i];
         if (key == sentinel) continue;
         const int64_t j = (int64_t)bucket_begin[key] + ranks[i];
         const PointRec r = rec[i];
-        if (blk == 0) {
-            // with the chord table built here, the tile kernel needs neither x nor y of the
-            // sorted record (the FP64 gates are in the chords): x carries the record's own
-            // sorted index, so the loader finds a candidate's chord row without a search
-            PointRec rs = r;
-            if (chords) rs.x = __int_as_float((int)j);
-            out[j] = rs;
-            if (bw_rec) bw_out[j] = bw_rec[i];
-        }
+        // with the chord table built here, the tile kernel needs neither x nor y of the
+        // sorted record (the FP64 gates are in the chords): x carries the record's own
+        // sorted index, so the loader finds a candidate's chord row without a search
+        PointRec rs = r;
+        if (chords) rs.x = __int_as_float((int)j);
+        out[j] = rs;
+        if (bw_rec) bw_out[j] = bw_rec[i];
         if (chords) {
             const GridParams g = bw_rec ? with_point_bw(gp, bw_rec[i]) : gp;
-            const int Y0 = ((r.Y - g.Hs) & ~7) + 8 * blk;
-            uint32_t w[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                w[k] = chord_entry(g, r, Y0 + 2 * k) | (chord_entry(g, r, Y0 + 2 * k + 1) << 16);
-            reinterpret_cast<uint4 *>(chords)[j * nb + blk] = make_uint4(w[0], w[1], w[2], w[3]);
+            const int Y0 = (r.Y - g.Hs) & ~7;
+            uint4 *dst = reinterpret_cast<uint4 *>(chords) + j * nb;
+            for (int blk = 0; blk < nb; ++blk) dst[blk] = chord_block(g, r, Y0 + 8 * blk);
         }
     }
 }
@@ -392,7 +408,7 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
     if (counting) {
         // bucket_begin[nbuckets] = the number of binned points
         const int nb = with_chords ? chord_rows(g.Hs) / 8 : 1;
-        const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n * nb + 255) / 256, (int64_t)p->num_sms * 32));
+        const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)p->num_sms * 32));
         k_scatter<<<blocks, 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin, (uint32_t)p->nbuckets, n,
                                           p->rec_sorted, ad ? p->bw_rec : nullptr, p->bw_sorted, g,
                                           with_chords ? p->chords : nullptr, nb);
@@ -417,9 +433,8 @@ __global__ void k_save_xy(const PointRec *__restrict__ rec, int64_t n, const uin
 }
 
 int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st, const float2 *xy) {
-    const int64_t total = n * (chord_rows(p->g.Hs) / 8);
-    if (total > 0) {
-        const unsigned blocks = (unsigned)std::min<int64_t>((total + 255) / 256, (int64_t)p->num_sms * 32);
+    if (n > 0) {
+        const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)p->num_sms * 32);
         k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr,
                                          p->bucket_begin + p->nbuckets, xy);
         p->last_own_launches += 1;
