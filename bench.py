@@ -352,13 +352,16 @@ def gpu_main(args, w, rank, world, local_rank):
         else:
             plan.compute_slab(p_pts, t0, t1, n_norm=w.n, out=out, stream=stream)
 
-    # N = 1, fixed variant: the step is ONE CUDA-graph launch of the captured pass
+    # fixed variant: the step is ONE CUDA-graph launch of the captured pass (the rank's slab)
     # (stkde_graph_create: binning, work list and tile kernel, ~20 kernels) -- the small grids
     # are launch-bound otherwise.  Same kernels, same work; --no-graph launches them one by one.
     graph = None
-    if world == 1 and variant == "fixed" and not args.no_graph:
+    if variant == "fixed" and not args.no_graph and t1 > t0:
         with torch.cuda.stream(stream):
-            graph = plan.graph(pts, out=out)
+            if xsplit:
+                graph = plan.graph_xslab(pts, x0, x1, n_norm=w.n, out=out) if x1 > x0 else None
+            else:
+                graph = plan.graph(pts, out=out, t_begin=t0, t_end=t1, n_norm=w.n)
 
     def step():
         if graph is not None:

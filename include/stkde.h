@@ -125,6 +125,9 @@ int stkde_compute_slab(stkde_plan_t plan, const float *d_points, int64_t n,
 typedef struct stkde_graph_s *stkde_graph_t;
 int stkde_graph_create(stkde_plan_t plan, const float *d_points, int64_t n, int64_t n_norm,
                        int64_t t_begin, int64_t t_end, float *d_out, stkde_graph_t *out);
+/* The same for one stkde_compute_xslab call (rows [x_begin, x_end) into d_xslab). */
+int stkde_graph_create_xslab(stkde_plan_t plan, const float *d_points, int64_t n, int64_t n_norm,
+                             int64_t x_begin, int64_t x_end, float *d_xslab, stkde_graph_t *out);
 int stkde_graph_launch(stkde_graph_t graph, void *stream);
 void stkde_graph_destroy(stkde_graph_t graph);
 

@@ -344,9 +344,9 @@ struct stkde_graph_s {
     int device;
 };
 
-extern "C" int stkde_graph_create(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm, int64_t t_begin,
-                                  int64_t t_end, float *d_out, stkde_graph_t *out) {
-    if (!p || !out) { set_error("NULL argument"); return STKDE_EINVAL; }
+// capture one enqueue sequence (fn(stream)) of plan p on a private stream into a CUDA graph
+template <class F>
+static int graph_capture(stkde_plan_s *p, stkde_graph_t *out, F fn) {
     *out = nullptr;
     CK(cudaSetDevice(p->device));
     cudaStream_t s;
@@ -357,7 +357,7 @@ extern "C" int stkde_graph_create(stkde_plan_t p, const float *d_points, int64_t
     cudaError_t e = cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
     int rc = STKDE_OK;
     if (e == cudaSuccess) {
-        rc = compute_slab_impl(p, d_points, n, n_norm, t_begin, t_end, d_out, s);
+        rc = fn(s);
         e = cudaStreamEndCapture(s, &graph);
     }
     p->timing = timing;
@@ -384,6 +384,22 @@ extern "C" int stkde_graph_create(stkde_plan_t p, const float *d_points, int64_t
     }
     *out = g;
     return STKDE_OK;
+}
+
+extern "C" int stkde_graph_create(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm, int64_t t_begin,
+                                  int64_t t_end, float *d_out, stkde_graph_t *out) {
+    if (!p || !out) { set_error("NULL argument"); return STKDE_EINVAL; }
+    return graph_capture(p, out, [&](cudaStream_t s) {
+        return compute_slab_impl(p, d_points, n, n_norm, t_begin, t_end, d_out, s);
+    });
+}
+
+extern "C" int stkde_graph_create_xslab(stkde_plan_t p, const float *d_points, int64_t n, int64_t n_norm,
+                                        int64_t x_begin, int64_t x_end, float *d_xslab, stkde_graph_t *out) {
+    if (!p || !out) { set_error("NULL argument"); return STKDE_EINVAL; }
+    return graph_capture(p, out, [&](cudaStream_t s) {
+        return stkde_compute_xslab(p, d_points, n, n_norm, x_begin, x_end, d_xslab, s);
+    });
 }
 
 extern "C" int stkde_graph_launch(stkde_graph_t g, void *stream) {
@@ -674,6 +690,44 @@ extern "C" int stkde_xslab_partition(stkde_plan_t p, const float *d_points, int6
     const GridParams &g = p->g;
     CK(cudaSetDevice(p->device));
     cudaStream_t st = (cudaStream_t)stream;
+    if (p->engine == STKDE_ENGINE_TC && n > 0 && n <= p->max_n) {
+        // tcgen05 engine: the cost of an x-tile column is the tile kernel's own work, its tiles'
+        // candidate counts (the same counts its work list sorts by) plus a fixed per-tile cost
+        // kappa (STKDE_XKAPPA), from one binning of the full grid.  Measured (one-GPU estimate of
+        // the 8-slab speedup, scripts/slab_scaling.py): kappa = 300 gives stress 6.45x and ornith
+        // 5.16x, kappa = 1000 6.17x and 5.57x, kappa = 3000 5.48x and 5.12x; the point histogram
+        // of stkde_xslab_cuts gives 6.45x and 5.31x.  Slab times vary +-5 % between runs.
+        int rc = launch_binning(p, d_points, n, st, 0, g.Gt, false);
+        if (rc) { set_error("binning launch failed"); return rc; }
+        const int nsl = g.NXA * g.NTY * g.NTT;
+        rc = launch_tile_cost(p, nsl, st);
+        if (rc) { set_error("tile-count launch failed"); return rc; }
+        std::vector<uint32_t> cnt((size_t)nsl);
+        CK(cudaMemcpyAsync(cnt.data(), p->tile_cnt, (size_t)nsl * 4, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double kappa = (double)env_int("STKDE_XKAPPA", 300);   // per-tile fixed cost, in candidates
+        std::vector<double> col(g.NTX, 0.0);
+        for (int ls = 0; ls < nsl; ++ls) col[ls % g.NXA + g.XA0] += kappa + (double)cnt[ls];
+        std::vector<double> cum(g.NTX + 1, 0.0);
+        for (int a = 0; a < g.NTX; ++a) cum[a + 1] = cum[a] + col[a];
+        const double tot = cum[g.NTX];
+        h_cuts[0] = 0;
+        int64_t prev = 0;
+        for (int k = 1; k < nparts; ++k) {
+            const double target = tot * k / nparts;
+            int64_t b = prev + 1;
+            while (b < g.NTX && cum[b] < target) ++b;
+            if (b > prev + 1 && (target - cum[b - 1]) < (cum[b] - target)) --b;
+            b = std::min<int64_t>(b, g.NTX - (nparts - k));
+            b = std::max<int64_t>(b, std::min<int64_t>(prev + 1, g.NTX));
+            h_cuts[k] = std::min<int64_t>(b * BX, g.Gx);
+            prev = b;
+        }
+        h_cuts[nparts] = g.Gx;
+        for (int k = 1; k <= nparts; ++k)
+            if (h_cuts[k] < h_cuts[k - 1]) h_cuts[k] = h_cuts[k - 1];
+        return STKDE_OK;
+    }
     std::vector<int> hist(g.Gx + 1, 0);
     if (n > 0) {
         int rc = launch_hist_x(p, d_points, n, st);

@@ -100,7 +100,7 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
     // culling most points of a slab call are unbinned, and one shared counter serialised them)
     // rank = this point's slot in its bucket (counting-sort path of the tcgen05 engine)
     const uint32_t rank = key != sentinel ? atomicAdd(&bucket_cnt[key], 1u) : 0u;
-    rec[i] = r;
+    if (key != sentinel) rec[i] = r;     // only binned records are read back (slab calls skip most)
     keys[i] = key;
     vals[i] = ranks ? rank : (uint32_t)i;
 }
@@ -473,6 +473,13 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
                                             p->max_slots, p->counters + 1);
     p->last_own_launches += 3;
     p->last_cub_calls += 2;
+    return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
+}
+
+// candidate count of every slab tile into p->tile_cnt (the x-slab partition's cost model)
+int launch_tile_cost(stkde_plan_s *p, int nsl, cudaStream_t st) {
+    k_tile_counts<<<nblk(nsl, 256), 256, 0, st>>>(p->g, p->bucket_begin, 0, nsl, p->lpt_key_in, p->lpt_val_in,
+                                                  p->tile_cnt, 0, 0u);
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
 }
 

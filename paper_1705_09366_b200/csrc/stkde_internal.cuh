@@ -241,6 +241,7 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
 int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st, const float2 *xy = nullptr);
 int launch_save_xy(stkde_plan_s *p, int64_t n, float2 *xy, cudaStream_t st);
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st);
+int launch_tile_cost(stkde_plan_s *p, int nsl, cudaStream_t st);
 int launch_tile(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float norm,
                 float *out, cudaStream_t st);
 int launch_count(stkde_plan_s *p, const float *d_points, int64_t n, int64_t t_begin,

@@ -26,7 +26,8 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_slab_partition", "stkde_slab_cuts", "stkde_count_contributions", "stkde_compute_sharded",
            "stkde_plan_check", "stkde_plan_info", "stkde_plan_enable_kernel_timing",
            "stkde_plan_kernel_ms", "stkde_plan_mma_stats", "stkde_plan_check_flags", "stkde_count_contributions_box",
-           "stkde_graph_create", "stkde_graph_launch", "stkde_graph_destroy", "stkde_strerror",
+           "stkde_graph_create", "stkde_graph_create_xslab", "stkde_graph_launch", "stkde_graph_destroy",
+           "stkde_strerror",
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
            "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
            "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x",
@@ -80,6 +81,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_check_flags.argtypes = [P, ctypes.POINTER(ctypes.c_uint32)]
     L.stkde_count_contributions_box.argtypes = [P, P, I64, I64, I64, I64, I64, P, P]
     L.stkde_graph_create.argtypes = [P, P, I64, I64, I64, I64, P, ctypes.POINTER(P)]
+    L.stkde_graph_create_xslab.argtypes = [P, P, I64, I64, I64, I64, P, ctypes.POINTER(P)]
     L.stkde_graph_launch.argtypes = [P, P]
     L.stkde_graph_destroy.argtypes = [P]
     L.stkde_graph_destroy.restype = None
@@ -109,7 +111,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_count_contributions", "stkde_compute_sharded", "stkde_plan_check",
                  "stkde_plan_info", "stkde_plan_enable_kernel_timing", "stkde_plan_kernel_ms",
                  "stkde_plan_mma_stats", "stkde_plan_check_flags", "stkde_count_contributions_box",
-                 "stkde_graph_create", "stkde_graph_launch", "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
+                 "stkde_graph_create", "stkde_graph_create_xslab", "stkde_graph_launch", "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
                  "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts",
                  "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x", "stkde_compute_f64",
                  "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64") + (DIAG if hasattr(L, DIAG[0]) else ()):
@@ -229,6 +231,19 @@ class Plan:
         h = ctypes.c_void_p()
         _check(load_library().stkde_graph_create(self._h, pts.data_ptr(), pts.shape[0], nn, int(t_begin), t1,
                                                  out.data_ptr(), ctypes.byref(h)))
+        return Graph(h, self, pts, out)
+
+    def graph_xslab(self, points: torch.Tensor, x_begin: int, x_end: int, n_norm: Optional[int] = None,
+                    out: Optional[torch.Tensor] = None) -> "Graph":
+        """Capture one compute_xslab call as a CUDA graph (stkde_graph_create_xslab)."""
+        pts = _points_arg(points, self.device)
+        if out is None:
+            out = torch.empty((int(x_end) - int(x_begin), self.G[1], self.G[2]), dtype=torch.float32,
+                              device=self.device)
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        h = ctypes.c_void_p()
+        _check(load_library().stkde_graph_create_xslab(self._h, pts.data_ptr(), pts.shape[0], nn, int(x_begin),
+                                                       int(x_end), out.data_ptr(), ctypes.byref(h)))
         return Graph(h, self, pts, out)
 
     # -- adaptive bandwidth (include/stkde.h; DESIGN.md reading R15) --

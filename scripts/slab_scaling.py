@@ -29,20 +29,22 @@ def timed(fn, reps=5):
     return e0.elapsed_time(e1) / reps
 
 
+# every step is one CUDA-graph launch (as bench.py times it)
 with S.Plan(max_n=w.n, device=0, **w.grid_kwargs()) as p:
     full = torch.empty(w.G, device=dev)
-    tf = timed(lambda: p.compute(t, out=full))
+    gfull = p.graph(t, out=full)
+    tf = timed(lambda: gfull.launch())
     for kind in ("t", "x"):
         for n in (2, 4, 8):
             cuts = p.slab_partition(t, n) if kind == "t" else p.xslab_partition(t, n)
             ts = []
             for a, b in zip(cuts[:-1], cuts[1:]):
                 if kind == "t":
-                    out = torch.empty((w.G[0], w.G[1], b - a), device=dev)
-                    ts.append(timed(lambda: p.compute_slab(t, a, b, n_norm=w.n, out=out)))
+                    gr = p.graph(t, t_begin=a, t_end=b, n_norm=w.n)
                 else:
-                    out = torch.empty((b - a, w.G[1], w.G[2]), device=dev)
-                    ts.append(timed(lambda: p.compute_xslab(t, a, b, n_norm=w.n, out=out)))
+                    gr = p.graph_xslab(t, a, b, n_norm=w.n)
+                ts.append(timed(lambda: gr.launch()))
+                gr.close()
             print("%s %s-slabs N=%d cuts=%s slab ms=%s -> ideal speedup %.2f (efficiency %.0f %%)" % (
                 name, kind, n, cuts, ["%.2f" % x for x in ts], tf / max(ts), 100 * tf / max(ts) / n))
     print("%s full grid %.2f ms" % (name, tf))

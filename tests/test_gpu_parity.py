@@ -411,6 +411,12 @@ def test_graph_capture_replays_compute(S, name):
         s = gs.launch().clone()
         torch.cuda.synchronize()
         assert torch.equal(s, direct2[:, :, t0:t1])
+        if p.info()["engine"] == 2:                         # x-slabs: tcgen05 engine
+            gx = p.graph_xslab(t, 16, min(48, g["Gx"]), n_norm=w.n)
+            sx = gx.launch().clone()
+            torch.cuda.synchronize()
+            assert torch.equal(sx, direct2[16:min(48, g["Gx"])])
+            gx.close()
         gr.close()
         gs.close()
         p.check()
