@@ -231,6 +231,15 @@ __global__ void k_scatter(const PointRec *__restrict__ rec, const uint32_t *__re
         // sorted index, so the loader finds a candidate's chord row without a search
         PointRec rs = r;
         if (chords) rs.x = __int_as_float((int)j);
+        if (chords && bw_rec) {
+            // adaptive: y carries the point's own reach for the loader's cull -- its disc radius
+            // rs_i = hs_i / sres rounded UP to 10 mantissa bits (conservative) with its window
+            // H_t(i) = floor(ht_i / tres) + 1 <= Ht in the 13 freed low bits
+            const PointBw b = bw_rec[i];
+            const int hti = min(gp.Ht, (int)(1.0f / b.inv_rt) + 1);
+            const uint32_t rb = (__float_as_uint(1.0f / b.inv_rs) + 0x1FFFu) & ~0x1FFFu;
+            rs.y = __uint_as_float(rb | (uint32_t)hti);
+        }
         out[j] = rs;
         if (bw_rec) bw_out[j] = bw_rec[i];
         if (chords) {
