@@ -187,13 +187,14 @@ __device__ __forceinline__ uint4 chord_block(const GridParams &g, const PointRec
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// (the sweep: xy != NULL holds the sorted points' world coordinates, and the record's x field
-// is set to its own sorted index for the tile kernel's loader, as in k_scatter)
+// Dense over the binned (sorted) points, so a slab call's few binned points cost only
+// themselves.  finalize: after its chords a record's x / y are rewritten for the loader (below);
+// the sweep (xy != NULL) keeps the world coordinates in a side buffer and sets x the same way.
 __global__ void k_chords(PointRec *__restrict__ rec, int64_t n, GridParams gp, uint16_t *__restrict__ chords,
                          const PointBw *__restrict__ bw, const uint32_t *__restrict__ nbinned,
-                         const float2 *__restrict__ xy) {
+                         const float2 *__restrict__ xy, int finalize) {
     const int nb = chord_rows(gp.Hs) / 8;            // 8-row blocks per point
-    const int64_t total = min(n, (int64_t)*nbinned);  // binned points only (they sort first)
+    const int64_t total = min(n, (int64_t)*nbinned);  // binned points only (they sort first): dense
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         PointRec r = rec[i];
         if (xy) {
@@ -206,6 +207,22 @@ __global__ void k_chords(PointRec *__restrict__ rec, int64_t n, GridParams gp, u
         const int Y0 = (r.Y - g.Hs) & ~7;
         uint4 *dst = reinterpret_cast<uint4 *>(chords) + i * nb;
         for (int blk = 0; blk < nb; ++blk) dst[blk] = chord_block(g, r, Y0 + 8 * blk);
+        if (finalize) {
+            // once the chords exist the tile kernel needs neither world coordinate of the sorted
+            // record (its FP64 gates are in the chords): x carries the record's own sorted index,
+            // so the loader finds a candidate's chord row without a search; adaptive calls: y
+            // carries the point's own reach for the loader's cull -- its disc radius
+            // rs_i = hs_i / sres rounded UP to 10 mantissa bits (conservative) with its window
+            // H_t(i) = floor(ht_i / tres) + 1 <= Ht in the 13 freed low bits
+            float2 xyw = make_float2(__int_as_float((int)i), r.y);
+            if (bw) {
+                const PointBw b = bw[i];
+                const int hti = min(gp.Ht, (int)(1.0f / b.inv_rt) + 1);
+                const uint32_t rb = (__float_as_uint(1.0f / b.inv_rs) + 0x1FFFu) & ~0x1FFFu;
+                xyw.y = __uint_as_float(rb | (uint32_t)hti);
+            }
+            reinterpret_cast<float2 *>(&rec[i].x)[0] = xyw;
+        }
     }
 }
 
@@ -213,41 +230,18 @@ __global__ void k_chords(PointRec *__restrict__ rec, int64_t n, GridParams gp, u
 // its slot from k_prep's atomic bucket count: buckets are contiguous runs as with the radix
 // sort, but the order inside a bucket is the atomics' order.  The tcgen05 tile sums are exact
 // integers, independent of the candidates' order and grouping, and every voxel is rounded
-// once from its sum, so the grid is bitwise the same for any order.  With
-// chords != NULL, thread (i, blk) also writes the point's chord block blk at the sorted
-// position (the k_chords table, fused: one pass over the records).
+// once from its sum, so the grid is bitwise the same for any order.  The chord
+// table follows in a dense pass over the sorted records (k_chords with finalize).
 __global__ void k_scatter(const PointRec *__restrict__ rec, const uint32_t *__restrict__ keys,
                           const uint32_t *__restrict__ ranks, const uint32_t *__restrict__ bucket_begin,
                           uint32_t sentinel, int64_t n, PointRec *__restrict__ out, const PointBw *__restrict__ bw_rec,
-                          PointBw *__restrict__ bw_out, GridParams gp, uint16_t *__restrict__ chords, int nb) {
-    // one thread per point (a 64-bit e / nb per (point, block) item cost more than the chords)
+                          PointBw *__restrict__ bw_out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t key = keys[i];
         if (key == sentinel) continue;
         const int64_t j = (int64_t)bucket_begin[key] + ranks[i];
-        const PointRec r = rec[i];
-        // with the chord table built here, the tile kernel needs neither x nor y of the
-        // sorted record (the FP64 gates are in the chords): x carries the record's own
-        // sorted index, so the loader finds a candidate's chord row without a search
-        PointRec rs = r;
-        if (chords) rs.x = __int_as_float((int)j);
-        if (chords && bw_rec) {
-            // adaptive: y carries the point's own reach for the loader's cull -- its disc radius
-            // rs_i = hs_i / sres rounded UP to 10 mantissa bits (conservative) with its window
-            // H_t(i) = floor(ht_i / tres) + 1 <= Ht in the 13 freed low bits
-            const PointBw b = bw_rec[i];
-            const int hti = min(gp.Ht, (int)(1.0f / b.inv_rt) + 1);
-            const uint32_t rb = (__float_as_uint(1.0f / b.inv_rs) + 0x1FFFu) & ~0x1FFFu;
-            rs.y = __uint_as_float(rb | (uint32_t)hti);
-        }
-        out[j] = rs;
+        out[j] = rec[i];
         if (bw_rec) bw_out[j] = bw_rec[i];
-        if (chords) {
-            const GridParams g = bw_rec ? with_point_bw(gp, bw_rec[i]) : gp;
-            const int Y0 = (r.Y - g.Hs) & ~7;
-            uint4 *dst = reinterpret_cast<uint4 *>(chords) + j * nb;
-            for (int blk = 0; blk < nb; ++blk) dst[blk] = chord_block(g, r, Y0 + 8 * blk);
-        }
     }
 }
 
@@ -416,14 +410,20 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
         return STKDE_ECUDA;
     if (counting) {
         // bucket_begin[nbuckets] = the number of binned points
-        const int nb = with_chords ? chord_rows(g.Hs) / 8 : 1;
-        const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)p->num_sms * 32));
-        k_scatter<<<blocks, 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin, (uint32_t)p->nbuckets, n,
-                                          p->rec_sorted, ad ? p->bw_rec : nullptr, p->bw_sorted, g,
-                                          with_chords ? p->chords : nullptr, nb);
-        p->ridx_in_rec = with_chords ? 1 : 0;
+        k_scatter<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin, (uint32_t)p->nbuckets,
+                                                 n, p->rec_sorted, ad ? p->bw_rec : nullptr, p->bw_sorted);
         p->last_own_launches += 2;
         p->last_cub_calls += 1;
+        p->ridx_in_rec = 0;
+        // the chord table over the binned (sorted, dense) points only: a slab call's few binned
+        // points are not spread over every warp of an all-points pass
+        if (with_chords) {
+            const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, (int64_t)p->num_sms * 64));
+            k_chords<<<blocks, 128, 0, st>>>(p->rec_sorted, n, g, p->chords, ad ? p->bw_sorted : nullptr,
+                                             p->bucket_begin + p->nbuckets, nullptr, 1);
+            p->ridx_in_rec = 1;
+            p->last_own_launches += 1;
+        }
     } else {
         p->ridx_in_rec = 0;
         // bucket_begin[nbuckets] = the number of binned points (the sentinel bucket sorts last)
@@ -445,7 +445,7 @@ int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st, const float2 *xy)
     if (n > 0) {
         const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)p->num_sms * 32);
         k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr,
-                                         p->bucket_begin + p->nbuckets, xy);
+                                         p->bucket_begin + p->nbuckets, xy, 0);
         p->last_own_launches += 1;
     }
     p->ridx_in_rec = xy ? 1 : 0;
