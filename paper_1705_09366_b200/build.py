@@ -46,11 +46,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
                     "-I", os.path.join(ROOT, "include")]
     if verbose:
         flags += ["-Xptxas", "-v"]
+    # the translation units compile in parallel (one nvcc each)
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC] + flags + ["-c", src, "-o", obj]
-        subprocess.check_call(cmd)
+        jobs.append([NVCC] + flags + ["-c", src, "-o", obj])
         objs.append(obj)
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        for f in [ex.submit(subprocess.check_call, cmd) for cmd in jobs]:
+            f.result()
     tmp = LIB + ".tmp%d" % os.getpid()
     subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"])
     os.replace(tmp, LIB)
