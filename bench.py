@@ -411,6 +411,17 @@ def gpu_main(args, w, rank, world, local_rank):
     kms, klaunch = plan.kernel_ms()
     plan.enable_kernel_timing(False)
     mma_cols, mma_kblocks = plan.mma_stats()
+    # per-phase device time (stkde_plan_enable_phase_timing: CUDA events at every phase end on
+    # the compute stream), from a separate untimed pass of the same steps launched one by one
+    plan.enable_phase_timing(True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            flush.fill_(1)
+            run(pts, bw)
+    barrier()
+    ph_ms, ph_calls = plan.phase_ms()
+    plan.enable_phase_timing(False)
+    phases = {k: round(v / max(args.steps, 1), 4) for k, v in ph_ms.items() if v > 0}
     ms = sum(ms_steps) / len(ms_steps)
     kernel_ms = kms / max(args.steps, 1)          # tile-kernel time per step (all its launches)
     vals = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
@@ -571,31 +582,28 @@ def gpu_main(args, w, rank, world, local_rank):
     gather = None
     if world > 1 and xsplit and variant == "fixed":
         full = torch.empty(tuple(w.G), dtype=torch.float32, device=dev) if rank == 0 else None
+        # the library's own NCCL communicator (stkde_plan_comm_init), id shipped over the group
+        uid = [S.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        plan.comm_init(world, rank, uid[0])
+        slab = out[:max(x1 - x0, 0)]
+
         def do_gather():
-            ops = []
-            if rank == 0:
-                full[x0:x1].copy_(out[:x1 - x0])
-                for r in range(1, world):
-                    a, b = xcuts[r], xcuts[r + 1]
-                    if b > a:
-                        ops.append(dist.P2POp(dist.irecv, full[a:b], r))
-            elif x1 > x0:
-                ops.append(dist.P2POp(dist.isend, out[:x1 - x0].contiguous(), 0))
-            if ops:
-                for q in dist.batch_isend_irecv(ops):
-                    q.wait()
+            with torch.cuda.stream(stream):
+                plan.gather_xslab(slab, xcuts, 0, full, stream=stream)
         do_gather()                                   # warm-up (NCCL P2P connection setup)
         barrier()
         gb_, ge_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        gb_.record()
+        gb_.record(stream)
         do_gather()
-        ge_.record()
+        ge_.record(stream)
         barrier()
         g_ms = torch.tensor([gb_.elapsed_time(ge_)], dtype=torch.float64, device=dev)
         dist.all_reduce(g_ms, op=dist.ReduceOp.MAX)
         gbytes = (w.G[0] - (x1 - x0 if rank == 0 else 0)) * w.G[1] * w.G[2] * 4
         gather = {"ms": float(g_ms.item()), "bytes_to_root": gbytes,
-                  "how": "NCCL batch_isend_irecv: each rank's x-slab into its rows of rank 0's grid",
+                  "how": "stkde_gather_xslab: NCCL send/recv group inside the library, each rank's x-slab "
+                         "received in place into its rows of rank 0's grid",
                   "timed_in_value": False}
         del full
 
@@ -633,6 +641,7 @@ def gpu_main(args, w, rank, world, local_rank):
             "clocks": clk.summary(),
             "roofline": roof,
             "roofline_tensor": roof_tc,
+            "phases_ms_per_step": phases,
             "engine": "FP64 gather tiles (stkde_tile_f64.cu)" if variant == "f64" else ENGINES[info["engine"]],
             "cpu_baseline": cpu,
         }

@@ -54,8 +54,9 @@ enum {
     STKDE_ECUDA = -3,       /* a CUDA runtime call failed                            */
     STKDE_ECAPACITY = -4,   /* n exceeds the plan's max_n                            */
     STKDE_ENONFINITE = -5,  /* some input coordinate was NaN/Inf (stkde_plan_check)  */
-    STKDE_EBANDWIDTH = -6   /* an adaptive call had a per-point bandwidth outside the
+    STKDE_EBANDWIDTH = -6,  /* an adaptive call had a per-point bandwidth outside the
                                plan's range (stkde_plan_check)                      */
+    STKDE_ENCCL = -7        /* NCCL unavailable or an NCCL call failed (gather)      */
 };
 
 /* Kernel pair (reading R1 in DESIGN.md). */
@@ -313,6 +314,67 @@ int stkde_plan_kernel_ms(stkde_plan_t plan, double *ms_total, int64_t *launches)
  * registers, two atomics per generator team when the persistent CTA exits); both are
  * reset.  Synchronises the device.  Zero for the other engines. */
 int stkde_plan_mma_stats(stkde_plan_t plan, int64_t *mma_columns, int64_t *kblocks);
+
+/* Per-phase device time of the pipeline (SURVEY.md §5 tracing; the GPU counterpart of
+ * the paper's init / compute breakdown, Fig. 6).  Phases, in enqueue
+ * order: PREP = point prep + home-bucket count (k_prep), SORT = the stable radix sort
+ * (FP32 engines and the FP64 path; 0 for the tcgen05 engine's counting sort), SCAN =
+ * bucket offsets, SCATTER = records into bucket order, CHORDS = the disc-chord table,
+ * WORKLIST = tile counts + order + chunking, TILES = the tile kernel, GATHER = the
+ * whole-grid gather (stkde_gather_*).  Every call also opens NVTX ranges named
+ * "stkde.<phase>" around the host-side enqueue of each phase (no cost without a tool). */
+enum {
+    STKDE_PHASE_PREP = 0,
+    STKDE_PHASE_SORT = 1,
+    STKDE_PHASE_SCAN = 2,
+    STKDE_PHASE_SCATTER = 3,
+    STKDE_PHASE_CHORDS = 4,
+    STKDE_PHASE_WORKLIST = 5,
+    STKDE_PHASE_TILES = 6,
+    STKDE_PHASE_GATHER = 7,
+    STKDE_NPHASES = 8
+};
+/* enable != 0: subsequent calls record a CUDA event on their stream at every phase end
+ * (skipped while the stream is being captured into a graph); resets the sums.
+ * stkde_plan_phase_ms writes the summed ms of each phase since enable to
+ * ms[STKDE_NPHASES] and the number of timed calls to *calls (synchronises on the last
+ * event).  stkde_phase_name(i) = "prep", "sort", ... (NULL outside [0, STKDE_NPHASES)).
+ * Errors: STKDE_EINVAL (NULL plan / ms), STKDE_ECUDA, STKDE_ENOMEM. */
+int stkde_plan_enable_phase_timing(stkde_plan_t plan, int enable);
+int stkde_plan_phase_ms(stkde_plan_t plan, double *ms, int64_t *calls);
+const char *stkde_phase_name(int phase);
+
+/* ---- NCCL gather of per-rank slabs (one process per GPU) ----
+ * The hot path has no collective (slabs are independent); the optional whole-grid
+ * gather to one rank runs inside the library over NCCL point-to-point (NVLink /
+ * NVSwitch).  NCCL is loaded at first use (dlopen "libnccl.so.2"); without it these
+ * calls return STKDE_ENCCL and everything else works.
+ *
+ * stkde_nccl_unique_id: rank 0 creates the 128-byte id (h_id, host) and ships it to the
+ * other ranks out of band (e.g. a torch.distributed broadcast).
+ * stkde_plan_comm_init: every rank creates the communicator on its plan's device
+ * (collective over the nranks ranks: each must call it; blocking).  The plan owns the
+ * communicator and destroys it in stkde_plan_destroy.  Re-init replaces it. */
+int stkde_nccl_unique_id(void *h_id /* 128 bytes */);
+int stkde_plan_comm_init(stkde_plan_t plan, int nranks, int rank, const void *h_id /* 128 bytes */);
+/* X-slab gather: rank r holds rows [h_cuts[r], h_cuts[r+1]) as float32 [rows][Gy][Gt]
+ * (stkde_compute_xslab).  Each is a contiguous block of the full grid, so the root
+ * receives every slab straight into d_full (float32 [Gx][Gy][Gt], root only; ignored on
+ * the other ranks) with no unpack; a root slab already in place (d_slab == its block
+ * of d_full) is not copied.  h_cuts (host, nranks+1 entries, ascending, 0 .. Gx) must be
+ * the same on every rank.  Collective over the communicator's ranks; asynchronous on
+ * `stream`.  Errors: STKDE_EINVAL (no communicator, bad cuts or root, NULL slab),
+ * STKDE_ENCCL (an NCCL call failed; stkde_last_error names it). */
+int stkde_gather_xslab(stkde_plan_t plan, const float *d_slab, const int64_t *h_cuts, int root, float *d_full,
+                       void *stream);
+/* Time-slab gather: rank r holds layers [h_cuts[r], h_cuts[r+1]) as float32
+ * [Gx][Gy][Ts] (stkde_compute_slab).  Slabs are strided in the T-innermost full grid,
+ * so the root receives the other ranks' slabs into a staging buffer the plan allocates
+ * on first use (sum of their sizes) and unpacks them with one kernel per slab; its own
+ * slab is unpacked straight from d_slab.  Same rules and errors as stkde_gather_xslab
+ * (plus STKDE_ENOMEM for the staging buffer). */
+int stkde_gather_slab(stkde_plan_t plan, const float *d_slab, const int64_t *h_cuts, int root, float *d_full,
+                      void *stream);
 
 /* Human-readable message for a return code / the last error of this thread. */
 const char *stkde_strerror(int code);

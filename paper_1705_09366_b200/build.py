@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         for f in [ex.submit(subprocess.check_call, cmd) for cmd in jobs]:
             f.result()
     tmp = LIB + ".tmp%d" % os.getpid()
-    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static"])
+    subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-cudart", "static", "-ldl"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -262,6 +262,7 @@ extern "C" void stkde_plan_destroy(stkde_plan_t p) {
     int cur = 0;
     cudaGetDevice(&cur);
     cudaSetDevice(p->device);
+    trace_comm_release(p);
     cudaFree(p->ws);
     for (int i = 0; i < 2 * p->tev_cap; ++i) cudaEventDestroy(p->tev[i]);
     free(p->tev);
@@ -325,9 +326,12 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
     const int c0 = (int)(t_begin / g.BT), c1 = (int)((t_end + g.BT - 1) / g.BT);
     rc = launch_worklist(p, c0, c1, st);
     if (rc) { set_error("work-list launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
-    rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
-         : p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
-                                            : launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
+    {
+        Phase ph(p, st, STKDE_PHASE_TILES);
+        rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
+             : p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
+                                                : launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
+    }
     if (rc) { set_error("tile kernel launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     return STKDE_OK;
 }
@@ -488,7 +492,10 @@ static int compute_f64_impl(stkde_plan_s *p, const float *d_points, const float 
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     // Alg. 1 divides the sum by n hs^2 ht; adaptive: terms carry 1/(hs_i^2 ht_i), the sum 1/n
     const double den = d_bw ? (double)n_norm : (double)n_norm * (g.hs * g.hs) * g.ht;
-    rc = launch_tile_f64(p, d_points, d_bw, t_begin, t_end, den, d_out, st);
+    {
+        Phase ph(p, st, STKDE_PHASE_TILES);
+        rc = launch_tile_f64(p, d_points, d_bw, t_begin, t_end, den, d_out, st);
+    }
     if (rc) { set_error("FP64 tile kernel launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     return STKDE_OK;
 }
@@ -583,10 +590,12 @@ extern "C" int stkde_compute_sweep(stkde_plan_t p, const float *d_points, int64_
         const float cnorm = (float)(kc / ((double)n * (h_hs[k] * h_hs[k]) * h_ht[k]));
         if (p->engine == STKDE_ENGINE_TC) rc = launch_chords(p, n, st, xy);
         if (!rc) rc = launch_worklist(p, c0, c1, st);
-        if (!rc)
+        if (!rc) {
+            Phase ph(p, st, STKDE_PHASE_TILES);
             rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)
                  : p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)
                                                     : launch_tile(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st);
+        }
         p->g = g0;
         if (rc) { set_error("sweep launch %d failed: %s", k, cudaGetErrorString(cudaGetLastError())); return rc; }
     }
@@ -1006,6 +1015,7 @@ extern "C" const char *stkde_strerror(int code) {
         case STKDE_ECAPACITY: return "n exceeds plan capacity (max_n)";
         case STKDE_ENONFINITE: return "non-finite point coordinate";
         case STKDE_EBANDWIDTH: return "per-point bandwidth outside the plan's range";
+        case STKDE_ENCCL: return "NCCL unavailable or an NCCL call failed";
     }
     return "unknown error";
 }

@@ -387,37 +387,50 @@ static inline unsigned nblk(int64_t n, int b) { return (unsigned)((n + b - 1) / 
 int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream_t st, int64_t t_begin,
                    int64_t t_end, bool with_chords, bool stable) {
     const GridParams &g = p->g;
-    cudaMemsetAsync(p->bucket_cnt, 0, (p->nbuckets + 1) * sizeof(uint32_t), st);
+    phase_call_begin(p, st);
     const bool ad = p->d_bw != nullptr;
     // tcgen05 engine: counting-sort scatter by the atomic bucket ranks (order-free exact sums);
     // the FP32 engines keep the stable radix sort (their sums depend on the order)
     // (stable: the FP64-output path sums each voxel in bucket-then-input order)
     const bool counting = p->engine == STKDE_ENGINE_TC && !stable;
-    if (ad) cudaMemsetAsync(p->counters + 6, 0, sizeof(int), st);
-    k_prep<<<nblk(n, 256), 256, 0, st>>>(d_points, n, g, p->rec, p->keys_in, p->vals_in, p->bucket_cnt,
-                                          p->counters + 1, (uint32_t)p->nbuckets, p->d_bw,
-                                          ad ? p->bw_rec : nullptr, reinterpret_cast<unsigned *>(p->counters + 6),
-                                          (int)t_begin, (int)t_end, counting ? 1 : 0);
+    {
+        Phase ph(p, st, STKDE_PHASE_PREP);
+        cudaMemsetAsync(p->bucket_cnt, 0, (p->nbuckets + 1) * sizeof(uint32_t), st);
+        if (ad) cudaMemsetAsync(p->counters + 6, 0, sizeof(int), st);
+        k_prep<<<nblk(n, 256), 256, 0, st>>>(d_points, n, g, p->rec, p->keys_in, p->vals_in, p->bucket_cnt,
+                                              p->counters + 1, (uint32_t)p->nbuckets, p->d_bw,
+                                              ad ? p->bw_rec : nullptr, reinterpret_cast<unsigned *>(p->counters + 6),
+                                              (int)t_begin, (int)t_end, counting ? 1 : 0);
+    }
     size_t bytes = p->cub_bytes;
     if (!counting) {
+        Phase ph(p, st, STKDE_PHASE_SORT);
         if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->keys_in, p->keys_out, p->vals_in, p->vals_out,
                                             (int)n, 0, p->key_bits, st) != cudaSuccess)
             return STKDE_ECUDA;
         bytes = p->cub_bytes;
     }
-    if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->bucket_cnt, p->bucket_begin, (int)(p->nbuckets + 1), st) !=
-        cudaSuccess)
-        return STKDE_ECUDA;
+    {
+        Phase ph(p, st, STKDE_PHASE_SCAN);
+        if (cub::DeviceScan::ExclusiveSum(p->cub_tmp, bytes, p->bucket_cnt, p->bucket_begin, (int)(p->nbuckets + 1),
+                                          st) != cudaSuccess)
+            return STKDE_ECUDA;
+    }
     if (counting) {
         // bucket_begin[nbuckets] = the number of binned points
-        k_scatter<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin, (uint32_t)p->nbuckets,
-                                                 n, p->rec_sorted, ad ? p->bw_rec : nullptr, p->bw_sorted);
+        {
+            Phase ph(p, st, STKDE_PHASE_SCATTER);
+            k_scatter<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin,
+                                                     (uint32_t)p->nbuckets, n, p->rec_sorted,
+                                                     ad ? p->bw_rec : nullptr, p->bw_sorted);
+        }
         p->last_own_launches += 2;
         p->last_cub_calls += 1;
         p->ridx_in_rec = 0;
         // the chord table over the binned (sorted, dense) points only: a slab call's few binned
         // points are not spread over every warp of an all-points pass
         if (with_chords) {
+            Phase ph(p, st, STKDE_PHASE_CHORDS);
             const unsigned blocks = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 127) / 128, (int64_t)p->num_sms * 64));
             k_chords<<<blocks, 128, 0, st>>>(p->rec_sorted, n, g, p->chords, ad ? p->bw_sorted : nullptr,
                                              p->bucket_begin + p->nbuckets, nullptr, 1);
@@ -427,6 +440,7 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
     } else {
         p->ridx_in_rec = 0;
         // bucket_begin[nbuckets] = the number of binned points (the sentinel bucket sorts last)
+        Phase ph(p, st, STKDE_PHASE_SCATTER);
         k_permute<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->vals_out, p->rec_sorted, n, ad ? p->bw_rec : nullptr,
                                                  p->bw_sorted, p->bucket_begin + p->nbuckets);
         p->last_own_launches += 2;
@@ -442,6 +456,7 @@ __global__ void k_save_xy(const PointRec *__restrict__ rec, int64_t n, const uin
 }
 
 int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st, const float2 *xy) {
+    Phase ph(p, st, STKDE_PHASE_CHORDS);
     if (n > 0) {
         const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, (int64_t)p->num_sms * 32);
         k_chords<<<blocks, 256, 0, st>>>(p->rec_sorted, n, p->g, p->chords, p->d_bw ? p->bw_sorted : nullptr,
@@ -453,6 +468,7 @@ int launch_chords(stkde_plan_s *p, int64_t n, cudaStream_t st, const float2 *xy)
 }
 
 int launch_save_xy(stkde_plan_s *p, int64_t n, float2 *xy, cudaStream_t st) {
+    Phase ph(p, st, STKDE_PHASE_SCATTER);
     if (n > 0) {
         k_save_xy<<<nblk(n, 256), 256, 0, st>>>(p->rec_sorted, n, p->bucket_begin + p->nbuckets, xy);
         p->last_own_launches += 1;
@@ -462,6 +478,7 @@ int launch_save_xy(stkde_plan_s *p, int64_t n, float2 *xy, cudaStream_t st) {
 
 int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
     const GridParams &g = p->g;
+    Phase ph(p, st, STKDE_PHASE_WORKLIST);
     int nsl = g.NXA * g.NTY * (c1 - c0);
     // locality order only for grids with many tiles per SM (few tiles: LPT balances the SMs)
     const int order = p->order >= 0 ? p->order : (nsl >= 64 * p->num_sms ? 1 : 0);
@@ -487,6 +504,7 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
 
 // candidate count of every slab tile into p->tile_cnt (the x-slab partition's cost model)
 int launch_tile_cost(stkde_plan_s *p, int nsl, cudaStream_t st) {
+    Phase ph(p, st, STKDE_PHASE_WORKLIST);
     k_tile_counts<<<nblk(nsl, 256), 256, 0, st>>>(p->g, p->bucket_begin, 0, nsl, p->lpt_key_in, p->lpt_val_in,
                                                   p->tile_cnt, 0, 0u);
     return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;

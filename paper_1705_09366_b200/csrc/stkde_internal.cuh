@@ -228,6 +228,20 @@ struct stkde_plan_s {
     double kernel_ms;
     int64_t kernel_launches;
     int last_own_launches, last_cub_calls;
+    // per-phase timing (stkde_plan_enable_phase_timing): events recorded at phase ends on the
+    // caller's stream, ph_id[k] = phase that ends at ph_ev[k] (-1: start of a call)
+    int ph_on;
+    cudaEvent_t *ph_ev;
+    int8_t *ph_id;
+    int ph_cap, ph_used;
+    double ph_ms[STKDE_NPHASES];
+    int64_t ph_calls;
+
+    // NCCL communicator of the per-rank gather (stkde_plan_comm_init; NULL until then)
+    void *comm;
+    int comm_rank, comm_nranks;
+    float *gather_stage;        // root's staging of the time-slab gather (lazily allocated)
+    size_t gather_stage_bytes;
 };
 
 namespace stkde {
@@ -265,4 +279,19 @@ int launch_tile_tc(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_e
 int launch_tile_f64(stkde_plan_s *p, const float *d_points, const float *d_bw, int64_t t_begin, int64_t t_end,
                     double den, double *out, cudaStream_t st);
 void set_error(const char *fmt, ...);
+// phase timing + NVTX ranges (stkde_trace_comm.cu): phase_call_begin marks the start of a
+// call on `st`; phase_begin opens the NVTX range of phase `ph`, phase_end closes it and
+// charges the interval since the previous mark on the plan to `ph`
+void phase_call_begin(stkde_plan_s *p, cudaStream_t st);
+void phase_begin(int ph);
+void phase_end(stkde_plan_s *p, cudaStream_t st, int ph);
+struct Phase {
+    stkde_plan_s *p;
+    cudaStream_t st;
+    int ph;
+    Phase(stkde_plan_s *p_, cudaStream_t st_, int ph_) : p(p_), st(st_), ph(ph_) { phase_begin(ph); }
+    ~Phase() { phase_end(p, st, ph); }
+};
+// frees the communicator, gather staging and phase events (stkde_plan_destroy)
+void trace_comm_release(stkde_plan_s *p);
 }  // namespace stkde

@@ -11,9 +11,11 @@ implicit and no reduction is needed: voxel tiles are independent.  There is NO
 collective on the data path, and every rank's slab is bitwise equal to the same
 block of a single-GPU run.
 
-`gather_slabs` is the optional whole-grid gather to one rank (NCCL point-to-
-point over NVLink on GPUs, gloo on CPU in the tests); `assemble` writes the
-slabs into the T-innermost full layout.  Neither is part of the timed hot path.
+The optional whole-grid gather to one rank runs inside the C library
+(`ShardedSTKDE.init_comm` + `gather`: stkde_plan_comm_init / stkde_gather_xslab /
+stkde_gather_slab, NCCL point-to-point over NVLink); `gather_slabs` + `assemble`
+are the torch.distributed alternative (any backend, gloo on CPU in the tests).
+Neither is part of the timed hot path.
 """
 from __future__ import annotations
 
@@ -22,7 +24,7 @@ from typing import List, Optional, Sequence
 import torch
 import torch.distributed as dist
 
-from .stkde import Plan
+from .stkde import Plan, nccl_unique_id
 
 
 def rank_slab(cuts: Sequence[int], rank: int):
@@ -89,6 +91,21 @@ class ShardedSTKDE:
         if self.s1 <= self.s0:
             return 0
         return int(self.plan.count_contributions(self.points, self.s0, self.s1).item())
+
+    def init_comm(self, group=None):
+        """Create the library's NCCL communicator for `gather` (rank 0's id shipped over `group`)."""
+        uid = [nccl_unique_id() if self.rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0, group=group)
+        self.plan.comm_init(self.world, self.rank, uid[0])
+
+    def gather(self, slab: torch.Tensor, root: int = 0, full: Optional[torch.Tensor] = None,
+               stream=None) -> Optional[torch.Tensor]:
+        """The whole grid on `root` (None elsewhere) by the library's NCCL gather; asynchronous."""
+        if self.rank == root and full is None:
+            full = torch.empty(self.G, dtype=torch.float32, device=self.points.device)
+        fn = self.plan.gather_xslab if self.axis == "x" else self.plan.gather_slab
+        fn(slab, self.cuts, root, full if self.rank == root else None, stream=stream)
+        return full if self.rank == root else None
 
     def close(self):
         self.plan.close()

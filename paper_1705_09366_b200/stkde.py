@@ -17,9 +17,11 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_PKG, "libstkde.so")
 
 STKDE_OK, STKDE_EINVAL, STKDE_ENOMEM, STKDE_ECUDA, STKDE_ECAPACITY, STKDE_ENONFINITE = 0, -1, -2, -3, -4, -5
-STKDE_EBANDWIDTH = -6
+STKDE_EBANDWIDTH, STKDE_ENCCL = -6, -7
 FLAG_NONFINITE, FLAG_WORKLIST, FLAG_BANDWIDTH = 1, 2, 4
 KERNEL_PRINTED, KERNEL_CLASSICAL = 0, 1
+# stkde_plan_phase_ms order (STKDE_PHASE_*)
+PHASES = ("prep", "sort", "scan", "scatter", "chords", "worklist", "tiles", "gather")
 
 # Exported entry points of include/stkde.h (checked by tests/test_abi.py).
 EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_compute_slab",
@@ -31,7 +33,9 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_last_error", "stkde_compute_adaptive", "stkde_compute_adaptive_slab",
            "stkde_count_contributions_adaptive", "stkde_compute_sweep", "stkde_compute_xslab",
            "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x",
-           "stkde_compute_f64", "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64")
+           "stkde_compute_f64", "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64",
+           "stkde_plan_enable_phase_timing", "stkde_plan_phase_ms", "stkde_phase_name",
+           "stkde_nccl_unique_id", "stkde_plan_comm_init", "stkde_gather_xslab", "stkde_gather_slab")
 
 
 class StkdeError(RuntimeError):
@@ -103,6 +107,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_compute_f64.argtypes = [P, P, I64, P, P]
     L.stkde_compute_slab_f64.argtypes = [P, P, I64, I64, I64, I64, P, P]
     L.stkde_compute_adaptive_slab_f64.argtypes = [P, P, P, I64, I64, I64, I64, P, P]
+    L.stkde_plan_enable_phase_timing.argtypes = [P, I32]
+    L.stkde_plan_phase_ms.argtypes = [P, ctypes.POINTER(D), ctypes.POINTER(I64)]
+    L.stkde_phase_name.argtypes = [I32]
+    L.stkde_phase_name.restype = ctypes.c_char_p
+    L.stkde_nccl_unique_id.argtypes = [P]
+    L.stkde_plan_comm_init.argtypes = [P, I32, I32, P]
+    L.stkde_gather_xslab.argtypes = [P, P, ctypes.POINTER(I64), I32, P, P]
+    L.stkde_gather_slab.argtypes = [P, P, ctypes.POINTER(I64), I32, P, P]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
@@ -114,7 +126,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_graph_create", "stkde_graph_create_xslab", "stkde_graph_launch", "stkde_compute_adaptive", "stkde_compute_adaptive_slab", "stkde_count_contributions_adaptive",
                  "stkde_compute_sweep", "stkde_compute_xslab", "stkde_xslab_partition", "stkde_xslab_cuts",
                  "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x", "stkde_compute_f64",
-                 "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64") + (DIAG if hasattr(L, DIAG[0]) else ()):
+                 "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64", "stkde_plan_enable_phase_timing",
+                 "stkde_plan_phase_ms", "stkde_nccl_unique_id", "stkde_plan_comm_init", "stkde_gather_xslab",
+                 "stkde_gather_slab") + (DIAG if hasattr(L, DIAG[0]) else ()):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -426,6 +440,46 @@ class Plan:
         _check(load_library().stkde_plan_kernel_ms(self._h, ctypes.byref(ms), ctypes.byref(k)))
         return ms.value, k.value
 
+    def enable_phase_timing(self, on: bool = True):
+        """CUDA events at every phase end of subsequent calls (stkde_plan_enable_phase_timing)."""
+        _check(load_library().stkde_plan_enable_phase_timing(self._h, 1 if on else 0))
+
+    def phase_ms(self):
+        """({phase: summed ms since enable}, timed calls) -- synchronises on the last event."""
+        ms = (ctypes.c_double * len(PHASES))()
+        k = ctypes.c_int64(0)
+        _check(load_library().stkde_plan_phase_ms(self._h, ms, ctypes.byref(k)))
+        return dict(zip(PHASES, list(ms))), k.value
+
+    # -- NCCL gather of per-rank slabs (one process per GPU) --
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """Create the plan's NCCL communicator (collective; uid from nccl_unique_id() on rank 0)."""
+        if len(uid) != 128:
+            raise ValueError("the NCCL unique id is 128 bytes")
+        buf = ctypes.create_string_buffer(uid, 128)
+        _check(load_library().stkde_plan_comm_init(self._h, int(nranks), int(rank), buf))
+
+    def _gather(self, fn, slab, cuts, root, full, stream):
+        if slab.dtype != torch.float32 or not slab.is_contiguous() or slab.device != self.device:
+            raise ValueError("slab must be a contiguous float32 tensor on the plan's device")
+        if full is not None and (full.dtype != torch.float32 or not full.is_contiguous()
+                                 or full.device != self.device or tuple(full.shape) != self.G):
+            raise ValueError("full must be a contiguous float32 (Gx, Gy, Gt) tensor on the plan's device")
+        c = (ctypes.c_int64 * len(cuts))(*[int(x) for x in cuts])
+        _check(fn(self._h, ctypes.c_void_p(slab.data_ptr()), c, int(root),
+                  ctypes.c_void_p(full.data_ptr()) if full is not None else None, _stream_ptr(stream, self.device)))
+        return full
+
+    def gather_xslab(self, slab: torch.Tensor, cuts: Sequence[int], root: int = 0,
+                     full: Optional[torch.Tensor] = None, stream=None):
+        """NCCL gather of every rank's x-slab into `full` on `root` (stkde_gather_xslab)."""
+        return self._gather(load_library().stkde_gather_xslab, slab, cuts, root, full, stream)
+
+    def gather_slab(self, slab: torch.Tensor, cuts: Sequence[int], root: int = 0,
+                    full: Optional[torch.Tensor] = None, stream=None):
+        """NCCL gather of every rank's time slab into `full` on `root` (stkde_gather_slab)."""
+        return self._gather(load_library().stkde_gather_slab, slab, cuts, root, full, stream)
+
     def tc_profile(self):
         """32 u64 phase counters of the tcgen05 kernel (STKDE_TC_PROF=1 at plan creation), reset on read."""
         buf = (ctypes.c_uint64 * 32)()
@@ -484,6 +538,13 @@ def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs
     fn = L.stkde_compute_sharded_x if axis == "x" else L.stkde_compute_sharded
     _check(fn(hp, nd, hpts, pts[0].shape[0], hsl, hc, int(root), None if full is None else full.data_ptr(), hs))
     return [int(c) for c in hc]
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte NCCL unique id (rank 0; ship it to the other ranks out of band)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().stkde_nccl_unique_id(buf))
+    return buf.raw
 
 
 def slab_cuts(G, Bt: int, Ht: int, rs: float, hist_T, nparts: int) -> list:

@@ -59,3 +59,18 @@ def test_product_does_not_import_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, re.M), f
                 assert "stkde_oracle" not in txt and "liboracle" not in txt, f
+
+
+def test_phase_names_and_nccl_id_without_gpu(lib_path):
+    # host-only calls: the phase names of stkde_plan_phase_ms and the NCCL unique id
+    import paper_1705_09366_b200 as S
+    L = S.load_library(lib_path)
+    assert tuple(L.stkde_phase_name(i).decode() for i in range(len(S.PHASES))) == S.PHASES
+    assert L.stkde_phase_name(len(S.PHASES)) is None and L.stkde_phase_name(-1) is None
+    assert b"NCCL" in L.stkde_strerror(S.STKDE_ENCCL)
+    try:
+        uid = S.nccl_unique_id()
+    except S.StkdeError as e:            # no NCCL in this process: the documented error
+        assert e.code == S.STKDE_ENCCL
+        return
+    assert len(uid) == 128 and uid != S.nccl_unique_id()
