@@ -403,6 +403,7 @@ def gpu_main(args, w, rank, world, local_rank):
         # replays no per-launch event records), CUDA events on the compute stream
         kms, klaunch = plan.kernel_ms()          # (resets nothing recorded inside the graph)
         plan.enable_kernel_timing(True)
+        plan.mma_stats()                        # issued-MMA counters: these K launches only
         with torch.cuda.stream(stream):
             for _ in range(args.steps):
                 flush.fill_(1)

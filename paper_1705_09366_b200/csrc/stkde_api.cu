@@ -253,6 +253,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     p->no_tma = env_int("STKDE_NO_TMA", 0);
     p->order = env_int("STKDE_ORDER", -1);       // -1: by the slab's tile count (launch_worklist)
     p->heavy = env_int("STKDE_HEAVY", p->chunk / 4);
+    p->wl_small = env_int("STKDE_WL_SMALL", 1);
     *out = p;
     return STKDE_OK;
 }

@@ -64,13 +64,12 @@ __device__ __forceinline__ bool make_bw(const GridParams &g, const float *__rest
 // K1: records, home-tile keys, bucket histogram.  Adaptive calls (bw != NULL) also
 // write the per-point bandwidths and the maximum normalisation weight
 // W_i = (sres/hs_i)^2 (tres/ht_i) (as float bits; positive floats order as unsigned).
-__global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, PointRec *__restrict__ rec,
-                       uint32_t *__restrict__ keys, uint32_t *__restrict__ vals,
-                       uint32_t *__restrict__ bucket_cnt, int *__restrict__ err, uint32_t sentinel,
-                       const float *__restrict__ bw, PointBw *__restrict__ bw_rec, unsigned *__restrict__ wmax,
-                       int t_begin, int t_end, int ranks) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+// one point: its record and home-bucket key (sentinel: not binned); writes bw_rec[i] and,
+// for a binned point, rec[i]
+__device__ __forceinline__ uint32_t prep_point(const float *__restrict__ pts, int64_t i, const GridParams &g,
+                                               PointRec *__restrict__ rec, int *__restrict__ err, uint32_t sentinel,
+                                               const float *__restrict__ bw, PointBw *__restrict__ bw_rec,
+                                               unsigned *__restrict__ wmax, int t_begin, int t_end) {
     float x = pts[3 * i], y = pts[3 * i + 1], t = pts[3 * i + 2];
     PointRec r;
     uint32_t key = sentinel;
@@ -87,7 +86,6 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
     }
     if (!make_rec(g, x, y, t, &r)) {
         atomicOr(err, 1);
-        r = PointRec{0, 0, 0, 0.f, 0.f, 0.f, 0.f, 0.f};
     } else if (bw_ok && reaches_grid(g, r) && r.T + g.Ht >= t_begin && r.T - g.Ht < t_end &&
                r.X + g.Hs >= g.XA0 * BX && r.X - g.Hs < (g.XA0 + g.NXA) * BX) {
         // (points whose window [T_i - H_t, T_i + H_t] misses the requested slab are not binned)
@@ -96,11 +94,22 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
         int c = min(max(r.T, 0), g.Gt - 1) / g.BTH;
         key = (uint32_t)((c * g.NTY + b) * g.NTX + a);
     }
+    if (key != sentinel) rec[i] = r;     // only binned records are read back (slab calls skip most)
+    return key;
+}
+
+__global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, PointRec *__restrict__ rec,
+                       uint32_t *__restrict__ keys, uint32_t *__restrict__ vals,
+                       uint32_t *__restrict__ bucket_cnt, int *__restrict__ err, uint32_t sentinel,
+                       const float *__restrict__ bw, PointBw *__restrict__ bw_rec, unsigned *__restrict__ wmax,
+                       int t_begin, int t_end, int ranks) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t key = prep_point(pts, i, g, rec, err, sentinel, bw, bw_rec, wmax, t_begin, t_end);
     // (unbinned points keep the sentinel key and sort last; they are not counted: with slab
     // culling most points of a slab call are unbinned, and one shared counter serialised them)
     // rank = this point's slot in its bucket (counting-sort path of the tcgen05 engine)
     const uint32_t rank = key != sentinel ? atomicAdd(&bucket_cnt[key], 1u) : 0u;
-    if (key != sentinel) rec[i] = r;     // only binned records are read back (slab calls skip most)
     keys[i] = key;
     vals[i] = ranks ? rank : (uint32_t)i;
 }
@@ -283,6 +292,67 @@ __global__ void k_tile_counts(GridParams g, const uint32_t *__restrict__ bucket_
 }
 
 // K3b: chunks per tile (in work-list order) packed with split-slot demand.
+// The whole work list of a small slab (nsl <= WL_CAP tiles) in ONE CTA, one tile per thread:
+// candidate counts, the keys' stable order by rank counting (each thread counts the keys
+// before its own: nsl broadcast shared-memory reads), chunk packing, the offset scan and the
+// items -- the six kernels of the general path (k_tile_counts, radix sort, k_chunk_pack,
+// scan, k_items) as one launch, for the launch-bound small grids (same keys, same order).
+constexpr int WL_THR = 1024, WL_CAP = WL_THR;
+__global__ void __launch_bounds__(WL_THR, 1)
+k_worklist_small(GridParams g, const uint32_t *__restrict__ bucket_begin, int c0, int nsl, int order,
+                 uint32_t heavy, int chunk, uint32_t *__restrict__ tcnt, uint32_t *__restrict__ lval,
+                 uint64_t *__restrict__ off_out, int4 *__restrict__ items, int64_t max_items, int64_t max_slots,
+                 int *__restrict__ err, int *__restrict__ work_counter) {
+    using Scan = cub::BlockScan<unsigned long long, WL_THR>;
+    __shared__ typename Scan::TempStorage ts;
+    __shared__ uint32_t skey[WL_CAP], scnt[WL_CAP], sid[WL_CAP];
+    const int ls = threadIdx.x;
+    uint32_t key = 0xFFFFFFFFu, cnt = 0;
+    if (ls < nsl) {
+        const int a = ls % g.NXA + g.XA0, b = (ls / g.NXA) % g.NTY, c = ls / (g.NXA * g.NTY) + c0;
+        cnt = tile_candidates(g, bucket_begin, a, b, c);
+        const uint32_t lpt = 0xFFFFu - min(cnt, 0xFFFFu);
+        key = (order == 0 || cnt >= heavy) ? lpt : 0x10000u + (uint32_t)ls;
+        tcnt[ls] = cnt;
+        skey[ls] = key;
+    }
+    __syncthreads();
+    if (ls < nsl) {                       // stable rank: keys below mine, and equal keys before me
+        int r = 0;
+        for (int q = 0; q < nsl; ++q) {
+            const uint32_t kq = skey[q];
+            r += (kq < key || (kq == key && q < ls)) ? 1 : 0;
+        }
+        lval[r] = (uint32_t)ls;
+        scnt[r] = cnt;
+        sid[r] = (uint32_t)ls;
+    }
+    __syncthreads();
+    unsigned long long pk = 0;
+    const int k = threadIdx.x;
+    if (k < nsl) {
+        const uint32_t c = scnt[k];
+        const uint32_t nch = c == 0 ? 1u : (c + chunk - 1) / chunk;
+        pk = (unsigned long long)nch | ((unsigned long long)(nch > 1 ? nch : 0) << 32);
+    }
+    unsigned long long o, total;
+    Scan(ts).ExclusiveSum(pk, o, total);
+    if (k < nsl) {
+        off_out[k] = o;
+        const uint32_t i0 = (uint32_t)o, nch = (uint32_t)pk, s0 = (uint32_t)(o >> 32);
+        if ((int64_t)i0 + nch > max_items || (nch > 1 && (int64_t)s0 + nch > max_slots)) {
+            atomicOr(err, 2);
+        } else {
+            const int tile = (int)sid[k];
+            for (uint32_t q = 0; q < nch; ++q)
+                items[i0 + q] = make_int4(tile, (int)q, (int)nch, nch > 1 ? (int)s0 : -1);
+        }
+    }
+    if (k == 0) {
+        off_out[nsl] = total;
+        *work_counter = 0;                // the tile kernel's item counter (no separate memset)
+    }
+}
 __global__ void k_chunk_pack(const uint32_t *__restrict__ lval, const uint32_t *__restrict__ tcnt, int nsl, int chunk,
                              uint64_t *__restrict__ pack) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
@@ -482,11 +552,20 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
     int nsl = g.NXA * g.NTY * (c1 - c0);
     // locality order only for grids with many tiles per SM (few tiles: LPT balances the SMs)
     const int order = p->order >= 0 ? p->order : (nsl >= 64 * p->num_sms ? 1 : 0);
-    k_tile_counts<<<nblk(nsl, 256), 256, 0, st>>>(g, p->bucket_begin, c0, nsl, p->lpt_key_in, p->lpt_val_in,
-                                                  p->tile_cnt, order, (uint32_t)p->heavy);
     int kbits = 16;                                  // LPT keys < 2^16; locality keys < 2^16 + nsl
     if (order != 0)
         while (kbits < 31 && (int64_t(1) << kbits) < 0x10000 + (int64_t)nsl) ++kbits;
+    if (nsl <= WL_CAP && p->wl_small) {              // small slab: the whole work list in one CTA
+        k_worklist_small<<<1, WL_THR, 0, st>>>(g, p->bucket_begin, c0, nsl, order, (uint32_t)p->heavy, p->chunk,
+                                               p->tile_cnt, p->lpt_val_out, p->chunk_off, p->items, p->max_items,
+                                               p->max_slots, p->counters + 1, p->counters);
+        p->wc_zeroed = 1;
+        p->last_own_launches += 1;
+        return cudaGetLastError() == cudaSuccess ? STKDE_OK : STKDE_ECUDA;
+    }
+    p->wc_zeroed = 0;
+    k_tile_counts<<<nblk(nsl, 256), 256, 0, st>>>(g, p->bucket_begin, c0, nsl, p->lpt_key_in, p->lpt_val_in,
+                                                  p->tile_cnt, order, (uint32_t)p->heavy);
     size_t bytes = p->cub_bytes;
     if (cub::DeviceRadixSort::SortPairs(p->cub_tmp, bytes, p->lpt_key_in, p->lpt_key_out, p->lpt_val_in,
                                         p->lpt_val_out, nsl, 0, kbits, st) != cudaSuccess)

@@ -204,6 +204,8 @@ struct stkde_plan_s {
     uint32_t *tile_cnt;         // [ntiles] candidate count per slab tile
     int order;                  // work-list order: 0 = LPT, 1 = heavy tiles by LPT, then locality, -1 = by size
     int heavy;                  // candidates from which a tile counts as heavy (order 1)
+    int wl_small;               // STKDE_WL_SMALL (default 1): one-CTA work list for small slabs
+    int wc_zeroed;              // the next tile launch's item counter was zeroed by k_worklist_small
     uint64_t *chunk_pack, *chunk_off;   // [ntiles + 1]
     int4 *items;                // [max_items]
     uint32_t *arrive;           // [ntiles]

@@ -461,7 +461,8 @@ int launch_tile_mma(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_
     const int64_t Ts = t_end - t_begin;
     const int vec_ok = (Ts % 4 == 0) && (t_begin % 4 == 0) && ((uintptr_t)out % 16 == 0);
     unsigned grid = (unsigned)std::min<int64_t>((int64_t)p->num_sms * p->ctas_per_sm, p->max_items);
-    cudaMemsetAsync(p->counters, 0, sizeof(int), st);
+    if (!p->wc_zeroed) cudaMemsetAsync(p->counters, 0, sizeof(int), st);   // (else by k_worklist_small)
+    p->wc_zeroed = 0;
     const bool timed = p->timing && p->tev_used < p->tev_cap;
     if (timed) cudaEventRecord(p->tev[2 * p->tev_used], st);
     f<<<grid, 256, p->smem_bytes, st>>>(g, p->rec_sorted, p->bucket_begin, p->items, p->chunk_off + nsl, p->counters,

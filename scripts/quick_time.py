@@ -32,8 +32,18 @@ for name in names:
         ms = e0.elapsed_time(e1) / K
         kms, kl = p.kernel_ms()
         info = p.info()
+        gr = p.graph(t, out=out)                     # the same call as one CUDA graph per step
+        for _ in range(3):
+            gr.launch()
+        e0.record()
+        for _ in range(K):
+            gr.launch()
+        e1.record()
+        torch.cuda.synchronize()
+        gms = e0.elapsed_time(e1) / K
+        gr.close()
         p.check()
-        print("%-7s n=%-8d C=%.3e  step %.3f ms  tile kernel %.3f ms  -> %.3e contrib/s  tile=%dx%dx%d CT=%d occ=%d chunk=%d launches=%d+%dcub eng=%d"
-              % (name, w.n, C, ms, kms / max(kl, 1), C / (ms * 1e-3), info["Bx"], info["By"], info["Bt"],
+        print("%-7s n=%-8d C=%.3e  step %.3f ms  graph %.4f ms  tile kernel %.3f ms  -> %.3e contrib/s  tile=%dx%dx%d CT=%d occ=%d chunk=%d launches=%d+%dcub eng=%d"
+              % (name, w.n, C, ms, gms, kms / max(kl, 1), C / (ms * 1e-3), info["Bx"], info["By"], info["Bt"],
                  info["tile_layers_per_thread"], info["tile_ctas_per_sm"], info["chunk_candidates"],
                  info["last_own_launches"], info["last_cub_calls"], info["engine"]), flush=True)
