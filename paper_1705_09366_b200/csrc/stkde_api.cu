@@ -105,7 +105,10 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     int BT, BYv;
     if (p->engine == STKDE_ENGINE_TC) {
         BYv = 8;
-        BT = Gt <= 64 ? 64 : 128;
+        // Bt = 64 for short grids, and for grids with fewer than 8 Bt = 128 tiles per SM: the
+        // persistent CTAs then hold several shorter tile pipelines each (dengue: 512 -> 1024 tiles)
+        const int64_t nt128 = ((Gx + BX - 1) / BX) * ((Gy + 7) / 8) * ((Gt + 127) / 128);
+        BT = (Gt <= 64 || nt128 < 8 * 148) ? 64 : 128;
     } else {
         BYv = BYW;
         BT = g.Ht >= 16 ? 64 : (g.Ht >= 6 ? 32 : 16);

@@ -293,10 +293,11 @@ __global__ void k_tile_counts(GridParams g, const uint32_t *__restrict__ bucket_
 
 // K3b: chunks per tile (in work-list order) packed with split-slot demand.
 // The whole work list of a small slab (nsl <= WL_CAP tiles) in ONE CTA, one tile per thread:
-// candidate counts, the keys' stable order by rank counting (each thread counts the keys
-// before its own: nsl broadcast shared-memory reads), chunk packing, the offset scan and the
-// items -- the six kernels of the general path (k_tile_counts, radix sort, k_chunk_pack,
-// scan, k_items) as one launch, for the launch-bound small grids (same keys, same order).
+// candidate counts, the keys' stable order (a bitonic sort of key << 10 | tile in shared
+// memory: ties keep the tile order, as the general path's stable radix sort does), chunk
+// packing, the offset scan and the items -- the six kernels of the general path
+// (k_tile_counts, radix sort, k_chunk_pack, scan, k_items) and the item-counter memset as
+// one launch, for the launch-bound small grids (same keys, same order, same items).
 constexpr int WL_THR = 1024, WL_CAP = WL_THR;
 __global__ void __launch_bounds__(WL_THR, 1)
 k_worklist_small(GridParams g, const uint32_t *__restrict__ bucket_begin, int c0, int nsl, int order,
@@ -305,35 +306,47 @@ k_worklist_small(GridParams g, const uint32_t *__restrict__ bucket_begin, int c0
                  int *__restrict__ err, int *__restrict__ work_counter) {
     using Scan = cub::BlockScan<unsigned long long, WL_THR>;
     __shared__ typename Scan::TempStorage ts;
-    __shared__ uint32_t skey[WL_CAP], scnt[WL_CAP], sid[WL_CAP];
+    __shared__ uint32_t sk[WL_CAP], scnt[WL_CAP];
     const int ls = threadIdx.x;
-    uint32_t key = 0xFFFFFFFFu, cnt = 0;
+    uint32_t cnt = 0, ck = 0xFFFFFFFFu;                        // padding sorts last
     if (ls < nsl) {
         const int a = ls % g.NXA + g.XA0, b = (ls / g.NXA) % g.NTY, c = ls / (g.NXA * g.NTY) + c0;
         cnt = tile_candidates(g, bucket_begin, a, b, c);
         const uint32_t lpt = 0xFFFFu - min(cnt, 0xFFFFu);
-        key = (order == 0 || cnt >= heavy) ? lpt : 0x10000u + (uint32_t)ls;
+        const uint32_t key = (order == 0 || cnt >= heavy) ? lpt : 0x10000u + (uint32_t)ls;   // < 2^17
+        ck = key << 10 | (uint32_t)ls;
         tcnt[ls] = cnt;
-        skey[ls] = key;
     }
-    __syncthreads();
-    if (ls < nsl) {                       // stable rank: keys below mine, and equal keys before me
-        int r = 0;
-        for (int q = 0; q < nsl; ++q) {
-            const uint32_t kq = skey[q];
-            r += (kq < key || (kq == key && q < ls)) ? 1 : 0;
+    scnt[ls] = cnt;
+    // ascending bitonic sort of the nsl keys padded to NP = 2^ceil(log2 nsl) (block-uniform):
+    // strides < 32 by warp shuffles, the others through shared memory
+    int NP = 32;
+    while (NP < nsl) NP <<= 1;
+    uint32_t v = ck;
+    for (int kk = 2; kk <= NP; kk <<= 1)
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+            uint32_t o;
+            if (jj >= 32) {
+                __syncthreads();                               // previous readers of sk done
+                sk[ls] = v;
+                __syncthreads();
+                o = sk[ls ^ jj];
+            } else {
+                o = __shfl_xor_sync(0xFFFFFFFFu, v, jj);
+            }
+            const bool up = (ls & kk) == 0, lower = (ls & jj) == 0;
+            v = (up == lower) ? min(v, o) : max(v, o);
         }
-        lval[r] = (uint32_t)ls;
-        scnt[r] = cnt;
-        sid[r] = (uint32_t)ls;
-    }
-    __syncthreads();
     unsigned long long pk = 0;
-    const int k = threadIdx.x;
+    const int k = ls;
+    int tile = 0;
+    __syncthreads();                                           // scnt complete
     if (k < nsl) {
-        const uint32_t c = scnt[k];
-        const uint32_t nch = c == 0 ? 1u : (c + chunk - 1) / chunk;
+        tile = (int)(v & 1023u);
+        const uint32_t cc = scnt[tile];
+        const uint32_t nch = cc == 0 ? 1u : (cc + chunk - 1) / chunk;
         pk = (unsigned long long)nch | ((unsigned long long)(nch > 1 ? nch : 0) << 32);
+        lval[k] = (uint32_t)tile;
     }
     unsigned long long o, total;
     Scan(ts).ExclusiveSum(pk, o, total);
@@ -343,7 +356,6 @@ k_worklist_small(GridParams g, const uint32_t *__restrict__ bucket_begin, int c0
         if ((int64_t)i0 + nch > max_items || (nch > 1 && (int64_t)s0 + nch > max_slots)) {
             atomicOr(err, 2);
         } else {
-            const int tile = (int)sid[k];
             for (uint32_t q = 0; q < nch; ++q)
                 items[i0 + q] = make_int4(tile, (int)q, (int)nch, nch > 1 ? (int)s0 : -1);
         }

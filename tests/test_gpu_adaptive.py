@@ -78,10 +78,13 @@ def run_adaptive(S, pts, bw, kernel=0, **g):
 
 
 @pytest.mark.parametrize("name,n,g,kernel", CASES, ids=[c[0] for c in CASES])
-def test_adaptive_parity(S, oracle_mod, name, n, g, kernel):
+def test_adaptive_parity(S, oracle_mod, name, n, g, kernel, monkeypatch):
+    if "bt128" in name:        # small grids default to Bt = 64
+        monkeypatch.setenv("STKDE_BT", "128")
     pts, bw = make_case(n, g, seed=zlib.crc32(name.encode()) % 1000)
     gpu, C, info = run_adaptive(S, pts, bw, kernel=kernel, **g)
     assert info["engine"] == 2
+    assert info["Bt"] == (128 if "bt128" in name else 64)
     ref = oracle_mod.stkde_pb_adaptive(pts, bw, kernel=kernel, **g)
     assert ref.vol.max() > 0
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=name)
@@ -90,10 +93,12 @@ def test_adaptive_parity(S, oracle_mod, name, n, g, kernel):
 
 @pytest.mark.parametrize("seed", range(6))
 @pytest.mark.parametrize("case", [0, 1], ids=["bt128", "bt64"])
-def test_adaptive_parity_seeds(S, oracle_mod, case, seed):
+def test_adaptive_parity_seeds(S, oracle_mod, case, seed, monkeypatch):
     # weights W_i / W_max span 64x here: the unbiased fixed-point sum (ICOMP)
     # keeps the small-weight points inside the tolerance
     name, n, g, kernel = CASES[case]
+    if "bt128" in name:        # small grids default to Bt = 64
+        monkeypatch.setenv("STKDE_BT", "128")
     pts, bw = make_case(n, g, seed=seed)
     gpu, C, _ = run_adaptive(S, pts, bw, kernel=kernel, **g)
     ref = oracle_mod.stkde_pb_adaptive(pts, bw, kernel=kernel, **g)

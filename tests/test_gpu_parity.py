@@ -89,8 +89,10 @@ def engine(request):
 
 
 @pytest.mark.parametrize("case", SMALL, ids=[c[0] for c in SMALL])
-def test_small_full_parity(S, oracle_mod, case, engine):
+def test_small_full_parity(S, oracle_mod, case, engine, monkeypatch):
     name, n, g, kid, clustered = case
+    if "bt128" in name and engine == 2:   # small grids default to Bt = 64 (< 8 Bt-128 tiles per SM)
+        monkeypatch.setenv("STKDE_BT", "128")
     pts = make_points(n, g, clustered, seed=len(name))
     gpu, C, info = run_gpu(S, pts, kernel=kid, **g)
     assert info["engine"] == engine
@@ -236,12 +238,13 @@ def test_edge_cases(S, oracle_mod):
         assert e.value.code == -1
 
 
-def test_tc_tma_store_edges(S, oracle_mod):
+def test_tc_tma_store_edges(S, oracle_mod, monkeypatch):
     # tcgen05 engine, T-aligned output rows (Gt % 4 == 0 -> TMA tensor-store epilogue) on a
     # grid ragged in x, y and in the last T tile: the hardware-clipped box edges must match
     # the oracle; a 4-aligned slab (TMA path) and an unaligned one (fallback stores) must
     # equal the full grid's layers bitwise
     g = G(37, 29, 132, hs=5.0, ht=9.0)
+    monkeypatch.setenv("STKDE_BT", "128")
     pts = make_points(700, g, True, seed=31)
     gpu, C, info = run_gpu(S, pts, **g)
     assert info["engine"] == 2 and info["Bt"] == 128
@@ -366,10 +369,11 @@ def test_sharded_x_single_process_equals_full(S):
 
 
 @pytest.mark.parametrize("case", [c for c in SMALL if c[0].startswith("classical_bt128")], ids=lambda c: c[0])
-def test_classical_bt128_slabs(S, oracle_mod, case):
+def test_classical_bt128_slabs(S, oracle_mod, case, monkeypatch):
     # the classical kernel on Bt = 128 tiles (both loader instantiations) through
     # the slab calls: every slab equals the full grid's layers bitwise, the full grid the oracle
     name, n, g, kid, clustered = case
+    monkeypatch.setenv("STKDE_BT", "128")
     pts = make_points(n, g, clustered, seed=len(name))
     dev = torch.device("cuda", 0)
     with S.Plan(max_n=len(pts), kernel=kid, device=0, **g) as p:
