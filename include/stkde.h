@@ -72,9 +72,12 @@ enum {
  * §3.5.  TC: the same contraction on 5th-generation tensor cores (tcgen05.mma
  * kind::i8, 23-bit fixed-point factors split into three 8-bit limbs, exact S32
  * accumulation in TMEM; M = 128 columns of a 16x8-column tile, A generated
- * into TMEM) -- DESIGN.md §3.5.  Hs > 120 falls back to TENSOR.  All engines compute the same sums
- * within the parity tolerance; they differ in speed only. */
-enum { STKDE_ENGINE_SIMT = 0, STKDE_ENGINE_TENSOR = 1, STKDE_ENGINE_TC = 2 };
+ * into TMEM) -- DESIGN.md §3.5.  Hs > 120 falls back to TENSOR.  WS: short temporal windows
+ * (H_t <= 8, H_s <= 120): FP32 FFMA2 accumulation of each point's window only, 16x16 columns x
+ * 32 layers, two columns per thread, the window offset dispatched to compile-time accumulator
+ * indices; other bandwidths fall back to TC.  All engines compute the same
+ * sums within the parity tolerance; they differ in speed only. */
+enum { STKDE_ENGINE_SIMT = 0, STKDE_ENGINE_TENSOR = 1, STKDE_ENGINE_TC = 2, STKDE_ENGINE_WS = 3 };
 
 typedef struct stkde_plan_s *stkde_plan_t;
 

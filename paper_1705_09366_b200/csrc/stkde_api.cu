@@ -94,10 +94,13 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     g.Gx = (int)Gx; g.Gy = (int)Gy; g.Gt = (int)Gt;
     g.Hs = (int)Hs_d; g.Ht = (int)Ht_d;
     p->engine = env_int("STKDE_ENGINE", STKDE_ENGINE_TC);
-    if (p->engine != STKDE_ENGINE_SIMT && p->engine != STKDE_ENGINE_TENSOR && p->engine != STKDE_ENGINE_TC) {
+    if (p->engine != STKDE_ENGINE_SIMT && p->engine != STKDE_ENGINE_TENSOR && p->engine != STKDE_ENGINE_TC &&
+        p->engine != STKDE_ENGINE_WS) {
         set_error("bad STKDE_ENGINE"); free(p); return STKDE_EINVAL;
     }
     // the tcgen05 engine stores per-point chords as int8 offsets: H_s <= 120
+    // the short-window engine: windows of <= 17 layers (its instantiations) and the chord table
+    if (p->engine == STKDE_ENGINE_WS && (g.Ht > 8 || g.Hs > 120)) p->engine = STKDE_ENGINE_TC;
     if (p->engine == STKDE_ENGINE_TC && g.Hs > 120) p->engine = STKDE_ENGINE_TENSOR;
     // Tile shape (DESIGN.md §3.4/§3.6): SIMT and mma.sync engines 16x16 columns x Bt
     // from the temporal window 2H_t+1; tcgen05 engine 16x8 columns (UMMA M = 128)
@@ -109,14 +112,19 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
         // persistent CTAs then hold several shorter tile pipelines each (dengue: 512 -> 1024 tiles)
         const int64_t nt128 = ((Gx + BX - 1) / BX) * ((Gy + 7) / 8) * ((Gt + 127) / 128);
         BT = (Gt <= 64 || nt128 < 8 * 148) ? 64 : 128;
+    } else if (p->engine == STKDE_ENGINE_WS) {
+        BYv = 16;
+        BT = 32;                                   // the engine's accumulators per column
     } else {
         BYv = BYW;
         BT = g.Ht >= 16 ? 64 : (g.Ht >= 6 ? 32 : 16);
     }
-    BT = env_int("STKDE_BT", BT);
+    if (p->engine != STKDE_ENGINE_WS) BT = env_int("STKDE_BT", BT);
     int CT = BT >= 64 ? 16 : 8;
     CT = env_int("STKDE_CT", CT);
-    if (p->engine == STKDE_ENGINE_TC ? tile_tc_smem_bytes(BT) == 0 : tile_smem_bytes(BT, CT) == 0) {
+    if (p->engine == STKDE_ENGINE_TC   ? tile_tc_smem_bytes(BT) == 0
+        : p->engine == STKDE_ENGINE_WS ? tile_ws_smem_bytes(g.Ht) == 0
+                                       : tile_smem_bytes(BT, CT) == 0) {
         set_error("unsupported tile shape Bt=%d CT=%d for engine %d", BT, CT, p->engine); free(p); return STKDE_EINVAL;
     }
     g.BT = BT;
@@ -136,7 +144,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     // Home-bucket depth in T: the tcgen05 engine bins points into 16x8x32 (16 when
     // H_t <= 8) blocks so a tile fetches only the blocks its temporal reach meets;
     // the legacy engines bin by whole tiles.
-    g.BTH = p->engine == STKDE_ENGINE_TC ? (g.Ht <= 8 ? 16 : 32) : BT;
+    g.BTH = p->engine == STKDE_ENGINE_TC ? (g.Ht <= 8 ? 16 : 32) : p->engine == STKDE_ENGINE_WS ? 16 : BT;
     g.BTH = env_int("STKDE_BTH", g.BTH);
     if (g.BTH < 1) { set_error("bad STKDE_BTH"); free(p); return STKDE_EINVAL; }
     g.NTTH = (int)((Gt + g.BTH - 1) / g.BTH);
@@ -177,6 +185,11 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
             return STKDE_EINVAL;
         }
         chunk = std::min<int64_t>(std::max<int64_t>(env_int("STKDE_CHUNK", 16384), need), 16384);
+    } else if (p->engine == STKDE_ENGINE_WS) {
+        // short-window engine: small chunks split hot tiles over many CTAs (a chunk of a
+        // 16x16x32 tile costs ~ its candidates x 4 warps x ~30 instructions)
+        const int64_t need = (2 * cand_bound + slot_budget - 1) / slot_budget;
+        chunk = std::max<int64_t>(env_int("STKDE_CHUNK", 1024), need);
     }
     chunk = std::min<int64_t>(chunk, (int64_t)1 << 30);
     p->chunk = (int)chunk;
@@ -187,6 +200,10 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
         p->tile_threads = 256;
         p->smem_bytes = tile_tc_smem_bytes(BT);
         rc = tile_tc_occupancy(BT, kernel_kind, &p->ctas_per_sm);
+    } else if (p->engine == STKDE_ENGINE_WS) {
+        p->tile_threads = 128;
+        p->smem_bytes = tile_ws_smem_bytes(g.Ht);
+        rc = tile_ws_occupancy(g.Ht, kernel_kind, p->smem_bytes, &p->ctas_per_sm);
     } else if (p->engine == STKDE_ENGINE_TENSOR) {
         p->tile_threads = 256;
         p->smem_bytes = tile_mma_smem_bytes(BT);
@@ -216,7 +233,8 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     Part parts[] = {
         {(void **)&p->rec, nrec * sizeof(PointRec)},
         {(void **)&p->rec_sorted, nrec * sizeof(PointRec)},
-        {(void **)&p->chords, p->engine == STKDE_ENGINE_TC ? nrec * (size_t)chord_rows(g.Hs) * 2 : 0},
+        {(void **)&p->chords, (p->engine == STKDE_ENGINE_TC || p->engine == STKDE_ENGINE_WS)
+                                  ? nrec * (size_t)chord_rows(g.Hs) * 2 : 0},
         {(void **)&p->bw_rec, p->engine == STKDE_ENGINE_TC ? nrec * sizeof(PointBw) : 0},
         {(void **)&p->bw_sorted, p->engine == STKDE_ENGINE_TC ? nrec * sizeof(PointBw) : 0},
         {(void **)&p->keys_in, nrec * 4}, {(void **)&p->keys_out, nrec * 4},
@@ -327,12 +345,18 @@ static int compute_slab_impl(stkde_plan_s *p, const float *d_points, int64_t n, 
     int rc = launch_binning(p, d_points, n, st, slab_cull ? t_begin : 0, slab_cull ? t_end : (int64_t)g.Gt,
                             p->engine == STKDE_ENGINE_TC);
     if (rc) { set_error("binning launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
+    // short-window engine: the chord table over the stably sorted records
+    if (p->engine == STKDE_ENGINE_WS && (rc = launch_chords(p, n, st))) {
+        set_error("chord launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+        return rc;
+    }
     const int c0 = (int)(t_begin / g.BT), c1 = (int)((t_end + g.BT - 1) / g.BT);
     rc = launch_worklist(p, c0, c1, st);
     if (rc) { set_error("work-list launch failed: %s", cudaGetErrorString(cudaGetLastError())); return rc; }
     {
         Phase ph(p, st, STKDE_PHASE_TILES);
         rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
+             : p->engine == STKDE_ENGINE_WS     ? launch_tile_ws(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
              : p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, t_begin, t_end, cnorm, d_out, st)
                                                 : launch_tile(p, c0, c1, t_begin, t_end, cnorm, d_out, st);
     }
@@ -592,11 +616,12 @@ extern "C" int stkde_compute_sweep(stkde_plan_t p, const float *d_points, int64_
     for (int k = 0; k < nbw; ++k) {
         p->g = narrowed(g0, h_hs[k], h_ht[k]);
         const float cnorm = (float)(kc / ((double)n * (h_hs[k] * h_hs[k]) * h_ht[k]));
-        if (p->engine == STKDE_ENGINE_TC) rc = launch_chords(p, n, st, xy);
+        if (p->engine == STKDE_ENGINE_TC || p->engine == STKDE_ENGINE_WS) rc = launch_chords(p, n, st, xy);
         if (!rc) rc = launch_worklist(p, c0, c1, st);
         if (!rc) {
             Phase ph(p, st, STKDE_PHASE_TILES);
             rc = p->engine == STKDE_ENGINE_TC       ? launch_tile_tc(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)
+                 : p->engine == STKDE_ENGINE_WS     ? launch_tile_ws(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)
                  : p->engine == STKDE_ENGINE_TENSOR ? launch_tile_mma(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st)
                                                     : launch_tile(p, c0, c1, 0, g0.Gt, cnorm, d_grids[k], st);
         }
@@ -756,7 +781,10 @@ static int xslab_impl(stkde_plan_t p, const float *d_points, const float *d_bw, 
                       int64_t x_begin, int64_t x_end, float *d_xslab, void *stream) {
     if (!p) { set_error("plan is NULL"); return STKDE_EINVAL; }
     const GridParams g0 = p->g;
-    if (p->engine != STKDE_ENGINE_TC) { set_error("x-slabs need the tcgen05 engine"); return STKDE_EINVAL; }
+    if (p->engine != STKDE_ENGINE_TC && p->engine != STKDE_ENGINE_WS) {
+        set_error("x-slabs need the tcgen05 or the short-window engine");
+        return STKDE_EINVAL;
+    }
     if (x_begin < 0 || x_end > g0.Gx || x_begin >= x_end || x_begin % BX != 0 || (x_end % BX != 0 && x_end != g0.Gx)) {
         set_error("x-slab [x_begin, x_end) must satisfy 0 <= x_begin < x_end <= Gx with x_begin and x_end "
                   "(unless = Gx) multiples of 16");

@@ -177,7 +177,8 @@ struct stkde_plan_s {
     stkde::GridParams g;
     int kernel;
     int CT;                   // layers per thread of the tile kernel (4 columns x CT)
-    int engine;               // STKDE_ENGINE_*: 0 = FP32 FFMA2 (SIMT), 1 = mma.sync 3xFP16, 2 = tcgen05 3xFP16
+    int engine;               // STKDE_ENGINE_*: 0 = FP32 FFMA2 (SIMT), 1 = mma.sync 3xFP16, 2 = tcgen05 kind::i8,
+                              // 3 = short-window FP32 (WS)
     int tile_threads;
     int ctas_per_sm;
     int64_t max_n;
@@ -277,6 +278,10 @@ int launch_tile_mma(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_
 size_t tile_tc_smem_bytes(int BT);
 int tile_tc_occupancy(int BT, int kernel, int *ctas_per_sm);
 int launch_tile_tc(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float cscale, float *out,
+                   cudaStream_t st);
+size_t tile_ws_smem_bytes(int Ht);
+int tile_ws_occupancy(int Ht, int KK, size_t smem, int *ctas_per_sm);
+int launch_tile_ws(stkde_plan_s *p, int c0, int c1, int64_t t_begin, int64_t t_end, float cscale, float *out,
                    cudaStream_t st);
 int launch_tile_f64(stkde_plan_s *p, const float *d_points, const float *d_bw, int64_t t_begin, int64_t t_end,
                     double den, double *out, cudaStream_t st);

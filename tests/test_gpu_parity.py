@@ -77,7 +77,7 @@ def make_points(n, g, clustered, seed):
     return np.concatenate([p, extra]).astype(np.float32)
 
 
-@pytest.fixture(params=[2, 1, 0], ids=["tc", "mma", "simt"])
+@pytest.fixture(params=[2, 1, 0, 3], ids=["tc", "mma", "simt", "ws"])
 def engine(request):
     old = os.environ.get("STKDE_ENGINE")
     os.environ["STKDE_ENGINE"] = str(request.param)
@@ -95,7 +95,9 @@ def test_small_full_parity(S, oracle_mod, case, engine, monkeypatch):
         monkeypatch.setenv("STKDE_BT", "128")
     pts = make_points(n, g, clustered, seed=len(name))
     gpu, C, info = run_gpu(S, pts, kernel=kid, **g)
-    assert info["engine"] == engine
+    # the short-window engine takes H_t <= 8 (and H_s <= 120); other plans fall back to tcgen05
+    ht_vox = int(np.ceil(g["ht"] / g["tres"]))
+    assert info["engine"] == (2 if engine == 3 and ht_vox > 8 else engine)
     ref = oracle_mod.stkde_pb(pts, kernel=kid, **g)
     assert_parity(gpu, ref.vol, ref.slack, ref.amb, what=name)
     assert C == ref.contributions
@@ -312,14 +314,21 @@ def test_xslabs_equal_full_grid(S, name):
         p.check()
 
 
-def test_xslab_ragged_grid(S):
+@pytest.mark.parametrize("eng", [2, 3], ids=["tc", "ws"])
+def test_xslab_ragged_grid(S, oracle_mod, eng, monkeypatch):
     # ragged x / y / unaligned G_t: the last x-slab ends at G_x, slabs still equal the full grid
+    # (tcgen05 and short-window engines; the latter's grid also against the oracle)
+    monkeypatch.setenv("STKDE_ENGINE", str(eng))
     g = G(45, 33, 70, hs=5.5, ht=7.0)
     pts = make_points(800, g, True, seed=41)
     dev = torch.device("cuda", 0)
     with S.Plan(max_n=len(pts), device=0, **g) as p:
+        assert p.info()["engine"] == eng
         t = torch.from_numpy(pts).to(dev)
         full = p.compute(t).cpu().numpy()
+        if eng == 3:
+            ref = oracle_mod.stkde_pb(pts, **g)
+            assert_parity(full, ref.vol, ref.slack, ref.amb, what="ws ragged")
         for a, b in ((0, 16), (16, 45), (32, 45), (0, 45)):
             s = p.compute_xslab(t, a, b).cpu().numpy()
             assert np.array_equal(s, full[a:b]), (a, b)
