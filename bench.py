@@ -58,7 +58,7 @@ DTYPES = {0: "f32", 1: "f16", 2: "u8"}
 NUMERICS = {0: "FP32 FFMA2 accumulation, two-level summation",
             1: "3-term FP16 split (mma.sync m16n8k16), FP32 accumulation, two-level summation",
             2: "23-bit fixed-point factors as three u8 limbs (tcgen05.mma kind::i8), exact S32 accumulation, "
-               "one FP32 rounding per voxel; max |gpu - oracle| <= 6e-7 of max (DESIGN.md §5)"}
+               "each voxel rounded from its exact int64 sum (int64 -> float, x scale); max |gpu - oracle| <= 9e-7 of max (DESIGN.md §5)"}
 NUMERICS_F64 = ("FP64 gates and factors with Alg. 1's operation sequence, fma accumulation in FP64, float64 grid; "
                 "|gpu - oracle| <= 2 (n + 2) 2^-53 f per voxel, exact support (DESIGN.md §3.8)")
 CONFIG_INDEX = {"tiny": 0, "dengue": 1, "social": 2, "ornith": 3, "stress": 4}

@@ -32,9 +32,11 @@
  *   - Results are deterministic: identical inputs give bitwise identical
  *     grids.  A time slab (stkde_compute_slab) or x-slab (stkde_compute_xslab)
  *     is bitwise equal to the same block of the full-grid result: with the
- *     tcgen05 engine for any boundary (exact integer accumulation, one rounding
- *     per voxel), with the FP32 engines for time-slab boundaries that are
- *     multiples of the tile height Bt.
+ *     tcgen05 engine for any boundary (exact integer accumulation; each voxel
+ *     rounded from its exact sum: int64 -> float, then x scale), with the
+ *     short-window FP32 engine (WS) for any boundary (every voxel sums in
+ *     candidate order), with the other FP32 engines for time-slab boundaries
+ *     that are multiples of the tile height Bt.
  *   - Return codes: STKDE_OK (0) or a negative STKDE_E* value; the message
  *     of the most recent error on the calling thread is stkde_last_error().
  */
