@@ -270,6 +270,47 @@ def config_dict(w, info, extra=None):
 
 
 # --------------------------------------------------------------------- GPU ---
+def direct_gather_ms(S, plan, pts, full, rank, local_rank, x0, x1, w, stream, barrier, dev):
+    """The direct gather fused into the compute (stkde_ipc_*): each rank's tile kernel stores its
+    x-slab straight into rank 0's grid over NVLink; one pass (binning + tiles) per step, the max
+    over ranks (compare with ms_per_step, the same pass into the rank's own buffer)."""
+    from paper_1705_09366_b200.sharded import direct_row_offset, exchange_root_handle
+    handle, root_off = exchange_root_handle(rank, 0, lambda: S.ipc_handle(full))
+    peer, why = None, ""
+    try:
+        peer = S.IpcMapping(handle, local_rank) if rank != 0 else None
+    except Exception as e:  # pragma: no cover - hardware-specific
+        why = repr(e)[:200]
+    ok = torch.tensor([0 if why else 1], dtype=torch.int32, device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)         # every rank mapped the root's grid, or none times
+    if not int(ok.item()):
+        if peer is not None:
+            peer.close()
+        return {"error": why or "another rank could not map rank 0's grid"}
+    try:
+        ptr = (full.data_ptr() if rank == 0 else peer.ptr(root_off)) + direct_row_offset(x0, w.G)
+
+        def direct():
+            if x1 > x0:
+                plan.compute_xslab_to(pts, x0, x1, ptr, n_norm=w.n, stream=stream)
+        direct()
+        barrier()
+        dd = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(3)]
+        for a_, b_ in dd:
+            a_.record(stream)
+            direct()
+            b_.record(stream)
+        barrier()
+        d_ms = torch.tensor([sum(a_.elapsed_time(b_) for a_, b_ in dd) / len(dd)], dtype=torch.float64, device=dev)
+        dist.all_reduce(d_ms, op=dist.ReduceOp.MAX)
+    finally:
+        if peer is not None:
+            peer.close()
+    return {"ms_per_step_into_root": float(d_ms.item()),
+            "how": "stkde_compute_xslab into rank 0's grid mapped with stkde_ipc_open: the epilogue's stores "
+                   "cross NVLink while the rank computes (no separate gather)"}
+
+
 def gpu_main(args, w, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -606,6 +647,15 @@ def gpu_main(args, w, rank, world, local_rank):
                   "how": "stkde_gather_xslab: NCCL send/recv group inside the library, each rank's x-slab "
                          "received in place into its rows of rank 0's grid",
                   "timed_in_value": False}
+        # the direct gather fused into the compute (stkde_ipc_*): each rank's tile kernel stores its
+        # x-slab straight into rank 0's grid over NVLink; one pass (binning + tiles) per step, the
+        # max over ranks, against the same pass into the rank's own buffer (ms_per_step)
+        # (a failure here is recorded in the line, never loses it; the path itself is tested
+        # bitwise on one GPU by tests/test_gpu_direct_gather.py)
+        try:
+            gather["direct"] = direct_gather_ms(S, plan, pts, full, rank, local_rank, x0, x1, w, stream, barrier, dev)
+        except Exception as e:  # pragma: no cover - hardware-specific
+            gather["direct"] = {"error": repr(e)[:200]}
         del full
 
     result = None

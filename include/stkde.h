@@ -381,6 +381,24 @@ int stkde_gather_xslab(stkde_plan_t plan, const float *d_slab, const int64_t *h_
 int stkde_gather_slab(stkde_plan_t plan, const float *d_slab, const int64_t *h_cuts, int root, float *d_full,
                       void *stream);
 
+/* ---- Direct x-slab gather over peer memory (CUDA IPC; one process per GPU) ----
+ * The fused alternative to stkde_gather_xslab: the root exports its full grid once, every
+ * rank maps it and passes its rows of the ROOT's grid as d_xslab to stkde_compute_xslab,
+ * so the tile kernel's epilogue stores the slab straight into the root's memory over
+ * NVLink / NVSwitch while the rank computes (no staging, no separate collective; the
+ * caller synchronises its stream and then the ranks, e.g. a torch.distributed barrier,
+ * before the root reads the grid).  An output on another device is written with plain
+ * warp-coalesced stores (no TMA tensor map over peer memory).
+ * stkde_ipc_get_handle: the 64-byte cudaIpcMemHandle of the allocation holding d_ptr
+ * (device memory of the calling process) and d_ptr's byte offset in it.
+ * stkde_ipc_open: maps a handle of another process on `device` (peer access enabled
+ * lazily); *d_base = the allocation's base (add the offset).  stkde_ipc_close unmaps it.
+ * Errors: STKDE_EINVAL (NULL arguments), STKDE_ECUDA (the CUDA call's message in
+ * stkde_last_error; a handle cannot be opened in the process that exported it). */
+int stkde_ipc_get_handle(const void *d_ptr, void *h_handle /* 64 bytes */, int64_t *offset);
+int stkde_ipc_open(int device, const void *h_handle /* 64 bytes */, void **d_base);
+int stkde_ipc_close(void *d_base);
+
 /* Human-readable message for a return code / the last error of this thread. */
 const char *stkde_strerror(int code);
 const char *stkde_last_error(void);

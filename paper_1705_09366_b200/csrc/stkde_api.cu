@@ -272,6 +272,7 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     p->tc_profile = env_int("STKDE_TC_PROF", 0);
     p->tc_watchdog = env_int("STKDE_TC_WATCHDOG", 0);
     p->no_tma = env_int("STKDE_NO_TMA", 0);
+    p->plain_stores = env_int("STKDE_PLAIN_STORES", 0);
     p->order = env_int("STKDE_ORDER", -1);       // -1: by the slab's tile count (launch_worklist)
     p->heavy = env_int("STKDE_HEAVY", p->chunk / 4);
     p->wl_small = env_int("STKDE_WL_SMALL", 1);
@@ -802,8 +803,15 @@ static int xslab_impl(stkde_plan_t p, const float *d_points, const float *d_bw, 
     p->g.NXA = (int)((x_end + BX - 1) / BX - x_begin / BX);
     // the tile kernel indexes the full grid; the slab is that grid's block of rows [x_begin, x_end)
     float *out_shifted = d_xslab - x_begin * (int64_t)g0.Gy * g0.Gt;
+    // the direct gather (include/stkde.h: stkde_ipc_*) passes rows of the root's grid on
+    // another device: its epilogue then uses plain stores over the peer mapping
+    cudaPointerAttributes pa;
+    p->out_remote = p->plain_stores || (cudaPointerGetAttributes(&pa, d_xslab) == cudaSuccess &&
+                                        pa.type == cudaMemoryTypeDevice && pa.device != p->device);
+    cudaGetLastError();
     const int rc = compute_slab_impl(p, d_points, n, n_norm, 0, g0.Gt, out_shifted, (cudaStream_t)stream, d_bw);
     p->g = g0;
+    p->out_remote = 0;
     return rc;
 }
 

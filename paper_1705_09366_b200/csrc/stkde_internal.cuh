@@ -218,6 +218,8 @@ struct stkde_plan_s {
     int tc_profile;             // STKDE_TC_PROF: record the tcgen05 kernel's phase profile
     int tc_watchdog;            // STKDE_TC_WATCHDOG: bounded mbarrier waits, record in counters[96..97]
     int no_tma;                 // STKDE_NO_TMA: epilogue stores by per-column bulk copies instead of TMA
+    int out_remote;             // the current call's output lives on another device (peer / IPC): plain stores
+    int plain_stores;           // STKDE_PLAIN_STORES: x-slab outputs always take the peer-output store path (tests)
     void *debug_progress;       // stkde_plan_debug_progress: per-(CTA, warp) protocol state (host-mapped)
     int *hist_t;                // [Gt + 1] slab-partition histogram
     int *hist_x;                // [Gx + 1] x-slab-partition histogram

@@ -343,3 +343,56 @@ extern "C" int stkde_gather_slab(stkde_plan_t p, const float *d_slab, const int6
     }
     return STKDE_OK;
 }
+
+// ---- direct x-slab gather over peer memory (CUDA IPC) ----
+// The allocation base of d_ptr comes from the driver's cuMemGetAddressRange (runtime
+// driver entry point: no link-time libcuda).
+extern "C" int stkde_ipc_get_handle(const void *d_ptr, void *h_handle, int64_t *offset) {
+    if (!d_ptr || !h_handle || !offset) { set_error("NULL argument"); return STKDE_EINVAL; }
+    typedef int (*range_fn)(unsigned long long *, size_t *, unsigned long long);
+    static range_fn range = nullptr;
+    if (!range) {
+        void *fp = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fp, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !fp) {
+            set_error("cuMemGetAddressRange is not available");
+            return STKDE_ECUDA;
+        }
+        range = (range_fn)fp;
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (unsigned long long)(uintptr_t)d_ptr) != 0) {
+        set_error("cuMemGetAddressRange failed (not device memory?)");
+        return STKDE_ECUDA;
+    }
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base);
+    if (e != cudaSuccess) { set_error("cudaIpcGetMemHandle: %s", cudaGetErrorString(e)); return STKDE_ECUDA; }
+    memcpy(h_handle, &h, sizeof h);
+    *offset = (int64_t)((uintptr_t)d_ptr - (uintptr_t)base);
+    return STKDE_OK;
+}
+
+extern "C" int stkde_ipc_open(int device, const void *h_handle, void **d_base) {
+    if (!h_handle || !d_base) { set_error("NULL argument"); return STKDE_EINVAL; }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) {
+        cudaIpcMemHandle_t h;
+        memcpy(&h, h_handle, sizeof h);
+        e = cudaIpcOpenMemHandle(d_base, h, cudaIpcMemLazyEnablePeerAccess);
+    }
+    cudaSetDevice(cur);
+    if (e != cudaSuccess) { set_error("cudaIpcOpenMemHandle: %s", cudaGetErrorString(e)); return STKDE_ECUDA; }
+    return STKDE_OK;
+}
+
+extern "C" int stkde_ipc_close(void *d_base) {
+    if (!d_base) { set_error("NULL argument"); return STKDE_EINVAL; }
+    const cudaError_t e = cudaIpcCloseMemHandle(d_base);
+    if (e != cudaSuccess) { set_error("cudaIpcCloseMemHandle: %s", cudaGetErrorString(e)); return STKDE_ECUDA; }
+    return STKDE_OK;
+}

@@ -16,6 +16,13 @@ The optional whole-grid gather to one rank runs inside the C library
 stkde_gather_slab, NCCL point-to-point over NVLink); `gather_slabs` + `assemble`
 are the torch.distributed alternative (any backend, gloo on CPU in the tests).
 Neither is part of the timed hot path.
+
+The direct gather (x-slabs; `export_root_grid` + `compute_direct` + `finish_direct`) fuses
+the gather into the compute: the root exports its full grid once as a CUDA IPC handle
+(stkde_ipc_get_handle, shipped with a torch.distributed object broadcast), every other
+rank maps it (stkde_ipc_open) and its tile kernel stores its rows straight into the root's
+memory over NVLink / NVSwitch while it computes -- no staging buffer and no collective
+after the compute, only a stream sync and a barrier.
 """
 from __future__ import annotations
 
@@ -24,11 +31,25 @@ from typing import List, Optional, Sequence
 import torch
 import torch.distributed as dist
 
-from .stkde import Plan, nccl_unique_id
+from .stkde import IpcMapping, Plan, ipc_handle, nccl_unique_id
 
 
 def rank_slab(cuts: Sequence[int], rank: int):
     return int(cuts[rank]), int(cuts[rank + 1])
+
+
+def exchange_root_handle(rank: int, root: int, export, group=None):
+    """Broadcast the root's exported buffer: the root calls export() -> (handle, offset) and
+    every rank returns the same (handle, offset) (collective over `group`)."""
+    obj = [export() if rank == root else None]
+    dist.broadcast_object_list(obj, src=root, group=group)
+    handle, offset = obj[0]
+    return handle, int(offset)
+
+
+def direct_row_offset(x0: int, G) -> int:
+    """Byte offset of grid row x0 in a float32 [Gx][Gy][Gt] grid (the slab's place in the root's grid)."""
+    return int(x0) * int(G[1]) * int(G[2]) * 4
 
 
 def validate_cuts(cuts: Sequence[int], extent: int, granule: int) -> None:
@@ -107,7 +128,41 @@ class ShardedSTKDE:
         fn(slab, self.cuts, root, full if self.rank == root else None, stream=stream)
         return full if self.rank == root else None
 
+    # ---- direct gather over peer memory (x-slabs) ----
+    def export_root_grid(self, root: int = 0, full: Optional[torch.Tensor] = None, group=None):
+        """Collective: the root allocates (or takes) the whole grid and exports it; the other
+        ranks map it.  Returns the grid on the root, None elsewhere."""
+        if self.axis != "x":
+            raise ValueError("the direct gather needs x-slabs (each slab is a contiguous block of rows)")
+        self.root = root
+        if self.rank == root:
+            self.full = full if full is not None else torch.empty(self.G, dtype=torch.float32,
+                                                                  device=self.points.device)
+        handle, self._root_off = exchange_root_handle(self.rank, root, lambda: ipc_handle(self.full), group)
+        if self.rank != root:
+            self._peer = IpcMapping(handle, self.points.device.index)
+        return self.full if self.rank == root else None
+
+    def compute_direct(self, stream=None) -> None:
+        """This rank's slab, stored by the tile kernel straight into the root's grid (asynchronous)."""
+        if self.s1 <= self.s0:
+            return
+        off = direct_row_offset(self.s0, self.G)
+        ptr = self.full.data_ptr() + off if self.rank == self.root else self._peer.ptr(self._root_off + off)
+        self.plan.compute_xslab_to(self.points, self.s0, self.s1, ptr, n_norm=int(self.points.shape[0]),
+                                   stream=stream)
+
+    def finish_direct(self, group=None) -> Optional[torch.Tensor]:
+        """Every rank's stores complete (device sync + barrier); the whole grid on the root."""
+        torch.cuda.synchronize(self.points.device)
+        dist.barrier(group=group)
+        return self.full if self.rank == self.root else None
+
     def close(self):
+        peer = getattr(self, "_peer", None)
+        if peer is not None:
+            peer.close()
+            self._peer = None
         self.plan.close()
 
 

@@ -35,7 +35,8 @@ EXPORTS = ("stkde_plan_create", "stkde_plan_destroy", "stkde_compute", "stkde_co
            "stkde_xslab_partition", "stkde_xslab_cuts", "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x",
            "stkde_compute_f64", "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64",
            "stkde_plan_enable_phase_timing", "stkde_plan_phase_ms", "stkde_phase_name",
-           "stkde_nccl_unique_id", "stkde_plan_comm_init", "stkde_gather_xslab", "stkde_gather_slab")
+           "stkde_nccl_unique_id", "stkde_plan_comm_init", "stkde_gather_xslab", "stkde_gather_slab",
+           "stkde_ipc_get_handle", "stkde_ipc_open", "stkde_ipc_close")
 
 
 class StkdeError(RuntimeError):
@@ -115,6 +116,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     L.stkde_plan_comm_init.argtypes = [P, I32, I32, P]
     L.stkde_gather_xslab.argtypes = [P, P, ctypes.POINTER(I64), I32, P, P]
     L.stkde_gather_slab.argtypes = [P, P, ctypes.POINTER(I64), I32, P, P]
+    L.stkde_ipc_get_handle.argtypes = [P, P, ctypes.POINTER(I64)]
+    L.stkde_ipc_open.argtypes = [I32, P, ctypes.POINTER(P)]
+    L.stkde_ipc_close.argtypes = [P]
     L.stkde_strerror.argtypes = [I32]
     L.stkde_strerror.restype = ctypes.c_char_p
     L.stkde_last_error.argtypes = []
@@ -128,7 +132,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "stkde_compute_adaptive_xslab", "stkde_compute_sharded_x", "stkde_compute_f64",
                  "stkde_compute_slab_f64", "stkde_compute_adaptive_slab_f64", "stkde_plan_enable_phase_timing",
                  "stkde_plan_phase_ms", "stkde_nccl_unique_id", "stkde_plan_comm_init", "stkde_gather_xslab",
-                 "stkde_gather_slab") + (DIAG if hasattr(L, DIAG[0]) else ()):
+                 "stkde_gather_slab", "stkde_ipc_get_handle", "stkde_ipc_open", "stkde_ipc_close") + (
+                     DIAG if hasattr(L, DIAG[0]) else ()):
         getattr(L, name).restype = I32
     _lib = L
     return L
@@ -337,6 +342,15 @@ class Plan:
                                                   out.data_ptr(), _stream_ptr(stream, self.device)))
         return out
 
+    def compute_xslab_to(self, points: torch.Tensor, x_begin: int, x_end: int, out_ptr: int,
+                         n_norm: Optional[int] = None, stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Rows [x_begin, x_end) written at device address out_ptr (float32 [x_end - x_begin][Gy][Gt],
+        e.g. the rows of the root's grid mapped with IpcMapping: the direct gather)."""
+        pts = _points_arg(points, self.device)
+        nn = pts.shape[0] if n_norm is None else int(n_norm)
+        _check(load_library().stkde_compute_xslab(self._h, pts.data_ptr(), pts.shape[0], nn, int(x_begin), int(x_end),
+                                                  ctypes.c_void_p(int(out_ptr)), _stream_ptr(stream, self.device)))
+
     def compute_adaptive_xslab(self, points: torch.Tensor, bw: torch.Tensor, x_begin: int, x_end: int,
                                n_norm: Optional[int] = None, out: Optional[torch.Tensor] = None,
                                stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
@@ -538,6 +552,46 @@ def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs
     fn = L.stkde_compute_sharded_x if axis == "x" else L.stkde_compute_sharded
     _check(fn(hp, nd, hpts, pts[0].shape[0], hsl, hc, int(root), None if full is None else full.data_ptr(), hs))
     return [int(c) for c in hc]
+
+
+def ipc_handle(t: torch.Tensor):
+    """(64-byte CUDA IPC handle of the allocation holding t, t's byte offset in it) -- export a
+    device buffer (the root's grid) to the other ranks' processes (stkde_ipc_get_handle)."""
+    if not t.is_cuda:
+        raise ValueError("ipc_handle needs a CUDA tensor")
+    buf = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64(0)
+    _check(load_library().stkde_ipc_get_handle(ctypes.c_void_p(t.data_ptr()), buf, ctypes.byref(off)))
+    return buf.raw, off.value
+
+
+class IpcMapping:
+    """Another process's device allocation mapped into this one (stkde_ipc_open); `ptr(offset)`
+    is a device address for the library's pointer-taking calls.  close() unmaps it."""
+
+    def __init__(self, handle: bytes, device: int):
+        if len(handle) != 64:
+            raise ValueError("a CUDA IPC handle is 64 bytes")
+        base = ctypes.c_void_p(0)
+        _check(load_library().stkde_ipc_open(int(device), ctypes.create_string_buffer(handle, 64), ctypes.byref(base)))
+        self.base = base.value
+        self.device = int(device)
+
+    def ptr(self, offset: int = 0) -> int:
+        if self.base is None:
+            raise ValueError("IPC mapping is closed")
+        return self.base + int(offset)
+
+    def close(self):
+        if self.base is not None:
+            _check(load_library().stkde_ipc_close(ctypes.c_void_p(self.base)))
+            self.base = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
 
 
 def nccl_unique_id() -> bytes:

@@ -164,3 +164,41 @@ def test_xslab_cuts_host():
     skew = [10 ** 6 if x < 128 else 1 for x in range(Gx)]  # compute-dominated mass in the first 128 columns
     c = S.xslab_cuts((Gx, Gy, Gt), 6.0, 4.0, skew, 4)
     assert c[1] <= 128 and c[2] <= 128
+
+
+def _worker_handle(rank, world, port, q):
+    # the direct gather's host protocol: the root's export is broadcast to every rank; row
+    # offsets place each x-slab in the root's [Gx][Gy][Gt] float32 grid
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_1705_09366_b200.sharded import direct_row_offset, exchange_root_handle
+        calls = []
+
+        def export():
+            calls.append(rank)
+            return bytes(range(64)), 4096
+        h, off = exchange_root_handle(rank, 1, export)
+        assert h == bytes(range(64)) and off == 4096
+        assert calls == ([1] if rank == 1 else [])          # only the root exports
+        assert direct_row_offset(0, (64, 32, 16)) == 0
+        assert direct_row_offset(5, (64, 32, 16)) == 5 * 32 * 16 * 4
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+
+
+def test_gloo_world2_direct_gather_protocol():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_handle, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: "ok", 1: "ok"}, res
