@@ -51,14 +51,17 @@ METRIC = "point-voxel contributions/sec"
 UNIT = "contributions/s"
 FP32_NOMINAL_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12   # 74.4: SMs x FP32 lanes x 2 x max SM clock
 FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12    # 37.2: SMs x FP64 lanes x 2 x max SM clock
-ENGINES = {0: "SIMT FP32 FFMA2", 1: "mma.sync m16n8k16 3xFP16", 2: "tcgen05.mma kind::i8, exact S32"}
-KERNELS = {0: "stkde::k_tile<Bt=%d>", 1: "stkde::k_tile_mma<Bt=%d>", 2: "stkde::k_tile_tc<Bt=%d>"}
+ENGINES = {0: "SIMT FP32 FFMA2", 1: "mma.sync m16n8k16 3xFP16", 2: "tcgen05.mma kind::i8, exact S32",
+           3: "short-window FP32 FFMA2 (window-offset dispatch)"}
+KERNELS = {0: "stkde::k_tile<Bt=%d>", 1: "stkde::k_tile_mma<Bt=%d>", 2: "stkde::k_tile_tc<Bt=%d>",
+           3: "stkde::k_tile_ws<Bt=%d>"}
 # the arithmetic type of the contraction (not a precision claim; NUMERICS says what it means)
-DTYPES = {0: "f32", 1: "f16", 2: "u8"}
+DTYPES = {0: "f32", 1: "f16", 2: "u8", 3: "f32"}
 NUMERICS = {0: "FP32 FFMA2 accumulation, two-level summation",
             1: "3-term FP16 split (mma.sync m16n8k16), FP32 accumulation, two-level summation",
             2: "23-bit fixed-point factors as three u8 limbs (tcgen05.mma kind::i8), exact S32 accumulation, "
-               "each voxel rounded from its exact int64 sum (int64 -> float, x scale); max |gpu - oracle| <= 9e-7 of max (DESIGN.md §5)"}
+               "each voxel rounded from its exact int64 sum (int64 -> float, x scale); max |gpu - oracle| <= 9e-7 of max (DESIGN.md §5)",
+            3: "FP32 FFMA2 accumulation of each point's temporal window, every voxel in candidate order (DESIGN.md §3.11)"}
 NUMERICS_F64 = ("FP64 gates and factors with Alg. 1's operation sequence, fma accumulation in FP64, float64 grid; "
                 "|gpu - oracle| <= 2 (n + 2) 2^-53 f per voxel, exact support (DESIGN.md §3.8)")
 CONFIG_INDEX = {"tiny": 0, "dengue": 1, "social": 2, "ornith": 3, "stress": 4}
