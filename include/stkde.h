@@ -265,7 +265,11 @@ int stkde_compute_sharded(stkde_plan_t *plans, int ndev,
 /* X-slab counterpart of stkde_compute_sharded: d_slabs[d] receives rows
  * [h_cuts[d], h_cuts[d+1]) (float32 [rows][Gy][Gt]); cuts from stkde_xslab_partition
  * on plans[0] when h_cuts[0] < 0; the optional gather is one peer copy per device
- * (each x-slab is a contiguous block of the full grid).  Same stream/asynchrony rules. */
+ * (each x-slab is a contiguous block of the full grid).  d_slabs == NULL fuses the gather
+ * into the compute: each device's tile kernel stores its rows straight into d_full_grid on
+ * plans[root]'s device over peer memory (peer access is enabled by the call), with no slab
+ * buffers and no copies; streams[root] then waits for every device's stream.  Same
+ * stream/asynchrony rules. */
 int stkde_compute_sharded_x(stkde_plan_t *plans, int ndev, const float *const *d_points, int64_t n,
                             float *const *d_slabs, int64_t *h_cuts, int root, float *d_full_grid,
                             void *const *streams);

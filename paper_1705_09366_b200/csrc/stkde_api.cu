@@ -905,17 +905,52 @@ extern "C" int stkde_compute_sharded(stkde_plan_t *plans, int ndev, const float 
 extern "C" int stkde_compute_sharded_x(stkde_plan_t *plans, int ndev, const float *const *d_points, int64_t n,
                                        float *const *d_slabs, int64_t *h_cuts, int root, float *d_full_grid,
                                        void *const *streams) {
-    if (!plans || ndev < 1 || !d_points || !d_slabs || !h_cuts || !streams) { set_error("bad arguments"); return STKDE_EINVAL; }
+    // d_slabs == NULL: the fused gather -- every device's tile kernel stores its rows straight into
+    // d_full_grid on the root (peer access enabled here), no slab buffers and no copies
+    const bool fused = d_slabs == nullptr;
+    if (!plans || ndev < 1 || !d_points || !h_cuts || !streams || (fused && !d_full_grid)) {
+        set_error("bad arguments");
+        return STKDE_EINVAL;
+    }
     for (int d = 0; d < ndev; ++d)
         if (!plans[d]) { set_error("plans[%d] is NULL", d); return STKDE_EINVAL; }
+    if (fused && (root < 0 || root >= ndev)) { set_error("root out of range"); return STKDE_EINVAL; }
     if (h_cuts[0] < 0) {
         int rc = stkde_xslab_partition(plans[0], d_points[0], n, ndev, h_cuts, streams[0]);
         if (rc) return rc;
     }
     for (int d = 0; d < ndev; ++d) {
         if (h_cuts[d + 1] <= h_cuts[d]) continue;   // empty slab
-        int rc = stkde_compute_xslab(plans[d], d_points[d], n, n, h_cuts[d], h_cuts[d + 1], d_slabs[d], streams[d]);
+        float *dst = d_slabs ? d_slabs[d] : nullptr;
+        if (fused) {
+            const int rdev = plans[root]->device, ddev = plans[d]->device;
+            if (ddev != rdev) {
+                CK(cudaSetDevice(ddev));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(rdev, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                    set_error("peer access %d -> %d: %s", ddev, rdev, cudaGetErrorString(e));
+                    return STKDE_ECUDA;
+                }
+                cudaGetLastError();
+            }
+            dst = d_full_grid + h_cuts[d] * (int64_t)plans[root]->g.Gy * plans[root]->g.Gt;
+        }
+        int rc = stkde_compute_xslab(plans[d], d_points[d], n, n, h_cuts[d], h_cuts[d + 1], dst, streams[d]);
         if (rc) return rc;
+    }
+    if (fused) {   // the root's stream waits for every other device's stores
+        stkde_plan_s *pr = plans[root];
+        for (int d = 0; d < ndev; ++d) {
+            if (h_cuts[d + 1] <= h_cuts[d] || streams[d] == streams[root]) continue;
+            cudaEvent_t ev;
+            CK(cudaSetDevice(plans[d]->device));
+            CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            CK(cudaEventRecord(ev, (cudaStream_t)streams[d]));
+            CK(cudaSetDevice(pr->device));
+            CK(cudaStreamWaitEvent((cudaStream_t)streams[root], ev, 0));
+            cudaEventDestroy(ev);
+        }
+        return STKDE_OK;
     }
     if (d_full_grid) {
         if (root < 0 || root >= ndev) { set_error("root out of range"); return STKDE_EINVAL; }

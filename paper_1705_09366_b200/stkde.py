@@ -533,7 +533,7 @@ class Graph:
             pass
 
 
-def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs: Sequence[torch.Tensor],
+def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs: Optional[Sequence[torch.Tensor]],
                     cuts: Optional[Sequence[int]] = None, root: int = -1,
                     full: Optional[torch.Tensor] = None, streams=None, axis: str = "t") -> list:
     """Single-process multi-device driver (stkde_compute_sharded, or stkde_compute_sharded_x for
@@ -544,7 +544,8 @@ def compute_sharded(plans: Sequence[Plan], points: Sequence[torch.Tensor], slabs
     hp = (P * nd)(*[p.handle.value for p in plans])
     pts = [_points_arg(x, p.device) for x, p in zip(points, plans)]
     hpts = (P * nd)(*[x.data_ptr() for x in pts])
-    hsl = (P * nd)(*[s.data_ptr() for s in slabs])
+    # slabs=None with axis="x" and a full grid: the fused gather (stores straight into `full`)
+    hsl = None if slabs is None else (P * nd)(*[s.data_ptr() for s in slabs])
     hc = (ctypes.c_int64 * (nd + 1))(*([-1] * (nd + 1) if cuts is None else [int(c) for c in cuts]))
     if streams is None:
         streams = [torch.cuda.current_stream(p.device) for p in plans]

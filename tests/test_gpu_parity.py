@@ -372,6 +372,12 @@ def test_sharded_x_single_process_equals_full(S):
         torch.cuda.synchronize()
         assert used == cuts
         assert torch.equal(full, full_ref)
+        # the fused gather: no slab buffers, every device's kernel stores into the root's grid
+        full2 = torch.full_like(full_ref, float("nan"))
+        used2 = S.compute_sharded(plans, [t] * 3, None, cuts=cuts, root=0, full=full2, axis="x")
+        torch.cuda.synchronize()
+        assert used2 == cuts
+        assert torch.equal(full2, full_ref)
     finally:
         for p in plans:
             p.close()
