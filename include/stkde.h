@@ -88,8 +88,9 @@ typedef struct stkde_plan_s *stkde_plan_t;
  * world units (H_s = ceil(hs/sres), H_t = ceil(ht/tres)).
  * `max_n` bounds the point count of later calls and sizes the device
  * workspace, so compute calls never allocate.  The tile shape depends on the
- * engine (tcgen05: 16 x 8 columns x Bt = 64 or 128 layers; legacy engines: 16 x 16
- * columns x Bt = 16, 32 or 64 from H_t); read it back with stkde_plan_info.  Writes the
+ * engine (tcgen05: 16 x 8 columns x Bt = 64 or 128 layers; short-window FP32: 16 x 16
+ * columns x 32 layers; legacy engines: 16 x 16 columns x Bt = 16, 32 or 64 from H_t);
+ * read it back with stkde_plan_info.  Writes the
  * plan to *out.  Errors: STKDE_EINVAL (message names the field),
  * STKDE_ENOMEM, STKDE_ECUDA. */
 int stkde_plan_create(stkde_plan_t *out, int device,
