@@ -275,6 +275,19 @@ def test_large_bandwidth_falls_back(S, oracle_mod):
     assert C == ref.contributions
 
 
+@pytest.mark.parametrize("hs", [120.0, 119.5], ids=["hs120", "hs119.5"])
+def test_largest_tc_bandwidth(S, oracle_mod, hs):
+    # H_s = 120, the largest the tcgen05 engine's int8 chord offsets hold (and a non-integer
+    # radius just under it): the tcgen05 engine, parity with the oracle
+    g = G(260, 250, 40, hs=hs, ht=4.0)
+    pts = make_points(20, g, False, seed=int(hs))
+    gpu, C, info = run_gpu(S, pts, **g)
+    assert info["engine"] == 2
+    ref = oracle_mod.stkde_pb(pts, **g)
+    assert_parity(gpu, ref.vol, ref.slack, ref.amb, what="hs=%g" % hs)
+    assert C == ref.contributions
+
+
 def test_partition_finer_than_bt(S):
     # more parts than Bt blocks (tcgen05 engine): the cost-balanced cuts refine to 32-layer
     # multiples, no slab is empty, and every slab equals the full grid's layers bitwise
