@@ -56,6 +56,8 @@ SMALL = [
     ("big_disc", 200, G(80, 70, 40, hs=30.0, ht=6.0), 0, False),
     ("one_voxel_grid", 50, G(1, 1, 1, hs=2.0, ht=2.0), 0, False),
     ("thin_slab", 400, G(64, 64, 3, hs=4.0, ht=1.0), 0, True),
+    # bandwidths below one voxel: the disc / window holds at most the nearest voxel centre
+    ("sub_voxel_bandwidth", 3000, G(40, 30, 20, hs=0.3, ht=0.4), 0, True),
     # classical kernel on Bt = 128 tiles (Gt > 64): small disc (H_s < 16, the PF = 1
     # loader instantiation) and large disc (H_s >= 16)
     ("classical_bt128_small", 900, G(45, 37, 150, hs=5.0, ht=6.0), 1, True),
