@@ -154,9 +154,10 @@ def test_adaptive_bad_bandwidth_flagged(S, oracle_mod):
     assert_parity(out, ref.vol * scale, ref.slack * scale, ref.amb, what="skip-bad-bw")
 
 
-def test_adaptive_needs_tc_engine(S):
+@pytest.mark.parametrize("eng", ["1", "3"], ids=["mma", "ws"])
+def test_adaptive_needs_tc_engine(S, eng):
     old = os.environ.get("STKDE_ENGINE")
-    os.environ["STKDE_ENGINE"] = "1"
+    os.environ["STKDE_ENGINE"] = eng
     try:
         g = G(20, 20, 20)
         pts, bw = make_case(50, g, seed=1)
