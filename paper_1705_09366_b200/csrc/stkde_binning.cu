@@ -285,8 +285,9 @@ __global__ void k_tile_counts(GridParams g, const uint32_t *__restrict__ bucket_
     if (ls >= nsl) return;
     int a = ls % g.NXA + g.XA0, b = (ls / g.NXA) % g.NTY, c = ls / (g.NXA * g.NTY) + c0;
     uint32_t cnt = tile_candidates(g, bucket_begin, a, b, c);
-    const uint32_t lpt = 0xFFFFu - min(cnt, 0xFFFFu);
-    lkey[ls] = (order == 0 || cnt >= heavy) ? lpt : 0x10000u + (uint32_t)ls;
+    // locality order in 16-bit keys: the non-heavy tiles share the largest key, and the stable
+    // sort keeps them in slab-tile order (two radix passes instead of three)
+    lkey[ls] = order == 0 ? 0xFFFFu - min(cnt, 0xFFFFu) : (cnt >= heavy ? 0xFFFEu - min(cnt, 0xFFFEu) : 0xFFFFu);
     lval[ls] = (uint32_t)ls;
     tcnt[ls] = cnt;
 }
@@ -564,9 +565,7 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
     int nsl = g.NXA * g.NTY * (c1 - c0);
     // locality order only for grids with many tiles per SM (few tiles: LPT balances the SMs)
     const int order = p->order >= 0 ? p->order : (nsl >= 64 * p->num_sms ? 1 : 0);
-    int kbits = 16;                                  // LPT keys < 2^16; locality keys < 2^16 + nsl
-    if (order != 0)
-        while (kbits < 31 && (int64_t(1) << kbits) < 0x10000 + (int64_t)nsl) ++kbits;
+    const int kbits = 16;                            // LPT and locality keys < 2^16 (k_tile_counts)
     if (nsl <= WL_CAP && p->wl_small) {              // small slab: the whole work list in one CTA
         k_worklist_small<<<1, WL_THR, 0, st>>>(g, p->bucket_begin, c0, nsl, order, (uint32_t)p->heavy, p->chunk,
                                                p->tile_cnt, p->lpt_val_out, p->chunk_off, p->items, p->max_items,
