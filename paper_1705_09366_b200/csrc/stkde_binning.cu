@@ -82,7 +82,7 @@ __device__ __forceinline__ uint32_t prep_point(const float *__restrict__ pts, in
             const double ws = g.sres / (double)b.hs, wt = g.tres / (double)b.ht;
             atomicMax(wmax, __float_as_uint((float)(ws * ws * wt)));
         }
-        bw_rec[i] = b;
+        if (bw_rec) bw_rec[i] = b;
     }
     if (!make_rec(g, x, y, t, &r)) {
         atomicOr(err, 1);
@@ -94,7 +94,9 @@ __device__ __forceinline__ uint32_t prep_point(const float *__restrict__ pts, in
         int c = min(max(r.T, 0), g.Gt - 1) / g.BTH;
         key = (uint32_t)((c * g.NTY + b) * g.NTX + a);
     }
-    if (key != sentinel) rec[i] = r;     // only binned records are read back (slab calls skip most)
+    // only binned records are read back (slab calls skip most); the counting-sort path writes
+    // none here: its scatter recomputes each record from the point (k_scatter)
+    if (key != sentinel && rec) rec[i] = r;
     return key;
 }
 
@@ -105,7 +107,8 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
                        int t_begin, int t_end, int ranks) {
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
-    const uint32_t key = prep_point(pts, i, g, rec, err, sentinel, bw, bw_rec, wmax, t_begin, t_end);
+    const uint32_t key = prep_point(pts, i, g, ranks ? nullptr : rec, err, sentinel, bw, ranks ? nullptr : bw_rec,
+                                    wmax, t_begin, t_end);
     // (unbinned points keep the sentinel key and sort last; they are not counted: with slab
     // culling most points of a slab call are unbinned, and one shared counter serialised them)
     // rank = this point's slot in its bucket (counting-sort path of the tcgen05 engine)
@@ -241,16 +244,24 @@ __global__ void k_chords(PointRec *__restrict__ rec, int64_t n, GridParams gp, u
 // integers, independent of the candidates' order and grouping, and every voxel is rounded
 // once from its sum, so the grid is bitwise the same for any order.  The chord
 // table follows in a dense pass over the sorted records (k_chords with finalize).
-__global__ void k_scatter(const PointRec *__restrict__ rec, const uint32_t *__restrict__ keys,
+__global__ void k_scatter(const float *__restrict__ pts, GridParams g, const uint32_t *__restrict__ keys,
                           const uint32_t *__restrict__ ranks, const uint32_t *__restrict__ bucket_begin,
-                          uint32_t sentinel, int64_t n, PointRec *__restrict__ out, const PointBw *__restrict__ bw_rec,
+                          uint32_t sentinel, int64_t n, PointRec *__restrict__ out, const float *__restrict__ bw,
                           PointBw *__restrict__ bw_out) {
+    // each binned record recomputed from its point (the same FP64 prep as k_prep: bitwise the
+    // same record) and written once at its bucket slot -- k_prep stores only keys and ranks
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t key = keys[i];
         if (key == sentinel) continue;
         const int64_t j = (int64_t)bucket_begin[key] + ranks[i];
-        out[j] = rec[i];
-        if (bw_rec) bw_out[j] = bw_rec[i];
+        PointRec r;
+        make_rec(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], &r);
+        out[j] = r;
+        if (bw) {
+            PointBw b;
+            make_bw(g, bw, i, &b);
+            bw_out[j] = b;
+        }
     }
 }
 
@@ -503,9 +514,9 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
         // bucket_begin[nbuckets] = the number of binned points
         {
             Phase ph(p, st, STKDE_PHASE_SCATTER);
-            k_scatter<<<nblk(n, 256), 256, 0, st>>>(p->rec, p->keys_in, p->vals_in, p->bucket_begin,
-                                                     (uint32_t)p->nbuckets, n, p->rec_sorted,
-                                                     ad ? p->bw_rec : nullptr, p->bw_sorted);
+            k_scatter<<<nblk(n, 256), 256, 0, st>>>(d_points, g, p->keys_in, p->vals_in, p->bucket_begin,
+                                                     (uint32_t)p->nbuckets, n, p->rec_sorted, p->d_bw,
+                                                     p->bw_sorted);
         }
         p->last_own_launches += 2;
         p->last_cub_calls += 1;
