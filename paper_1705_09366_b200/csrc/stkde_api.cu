@@ -733,9 +733,11 @@ extern "C" int stkde_xslab_partition(stkde_plan_t p, const float *d_points, int6
         // tcgen05 engine: the cost of an x-tile column is the tile kernel's own work, its tiles'
         // candidate counts (the same counts its work list sorts by) plus a fixed per-tile cost
         // kappa (STKDE_XKAPPA), from one binning of the full grid.  Measured (one-GPU estimate of
-        // the 8-slab speedup, scripts/slab_scaling.py): kappa = 300 gives stress 6.45x and ornith
-        // 5.16x, kappa = 1000 6.17x and 5.57x, kappa = 3000 5.48x and 5.12x; the point histogram
-        // of stkde_xslab_cuts gives 6.45x and 5.31x.  Slab times vary +-5 % between runs.
+        // the 8-slab speedup, scripts/slab_scaling.py): round 1, kappa = 300 gave stress 6.45x and
+        // ornith 5.16x, kappa = 1000 6.17x and 5.57x, kappa = 3000 5.48x and 5.12x; the point
+        // histogram of stkde_xslab_cuts 6.45x and 5.31x.  Final round-2 build: kappa = 0 / 150 /
+        // 300 / 500 / 600 / 1200 give stress 6.65 / 6.66 / 6.96 / 6.85 / 6.85 / 6.57x and ornith
+        // 5.58 / 5.75 / 5.97 / 6.15 / 6.12 / 6.02x (500: both >= 6).  Slab times vary +-5 %.
         int rc = launch_binning(p, d_points, n, st, 0, g.Gt, false);
         if (rc) { set_error("binning launch failed"); return rc; }
         const int nsl = g.NXA * g.NTY * g.NTT;
@@ -744,7 +746,7 @@ extern "C" int stkde_xslab_partition(stkde_plan_t p, const float *d_points, int6
         std::vector<uint32_t> cnt((size_t)nsl);
         CK(cudaMemcpyAsync(cnt.data(), p->tile_cnt, (size_t)nsl * 4, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        const double kappa = (double)env_int("STKDE_XKAPPA", 300);   // per-tile fixed cost, in candidates
+        const double kappa = (double)env_int("STKDE_XKAPPA", 500);   // per-tile fixed cost, in candidates
         std::vector<double> col(g.NTX, 0.0);
         for (int ls = 0; ls < nsl; ++ls) col[ls % g.NXA + g.XA0] += kappa + (double)cnt[ls];
         std::vector<double> cum(g.NTX + 1, 0.0);
