@@ -112,9 +112,10 @@ __global__ void k_prep(const float *__restrict__ pts, int64_t n, GridParams g, P
     // (unbinned points keep the sentinel key and sort last; they are not counted: with slab
     // culling most points of a slab call are unbinned, and one shared counter serialised them)
     // rank = this point's slot in its bucket (counting-sort path of the tcgen05 engine)
-    const uint32_t rank = key != sentinel ? atomicAdd(&bucket_cnt[key], 1u) : 0u;
     keys[i] = key;
-    vals[i] = ranks ? rank : (uint32_t)i;
+    const uint32_t rank = key != sentinel ? atomicAdd(&bucket_cnt[key], 1u) : 0u;   // (every path's counts)
+    if (!ranks) vals[i] = (uint32_t)i;
+    else if (key != sentinel) vals[i] = rank;     // unbinned points' ranks are never read
 }
 
 // K1b: records (and adaptive bandwidths) in bucket order (coalesced candidate reads
@@ -250,17 +251,31 @@ __global__ void k_scatter(const float *__restrict__ pts, GridParams g, const uin
                           PointBw *__restrict__ bw_out) {
     // each binned record recomputed from its point (the same FP64 prep as k_prep: bitwise the
     // same record) and written once at its bucket slot -- k_prep stores only keys and ranks
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t key = keys[i];
-        if (key == sentinel) continue;
-        const int64_t j = (int64_t)bucket_begin[key] + ranks[i];
-        PointRec r;
-        make_rec(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], &r);
-        out[j] = r;
-        if (bw) {
-            PointBw b;
-            make_bw(g, bw, i, &b);
-            bw_out[j] = b;
+    // four keys per thread and iteration (one 16-B load): slab calls skip most points, so the
+    // key reads are the pass's main traffic
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t i0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; i0 < n; i0 += stride) {
+        uint32_t kk[4];
+        if (i0 + 4 <= n) {
+            const uint4 k4 = *reinterpret_cast<const uint4 *>(keys + i0);
+            kk[0] = k4.x; kk[1] = k4.y; kk[2] = k4.z; kk[3] = k4.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) kk[q] = i0 + q < n ? keys[i0 + q] : sentinel;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (kk[q] == sentinel) continue;
+            const int64_t i = i0 + q;
+            const int64_t j = (int64_t)bucket_begin[kk[q]] + ranks[i];
+            PointRec r;
+            make_rec(g, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2], &r);
+            out[j] = r;
+            if (bw) {
+                PointBw b;
+                make_bw(g, bw, i, &b);
+                bw_out[j] = b;
+            }
         }
     }
 }
@@ -514,7 +529,8 @@ int launch_binning(stkde_plan_s *p, const float *d_points, int64_t n, cudaStream
         // bucket_begin[nbuckets] = the number of binned points
         {
             Phase ph(p, st, STKDE_PHASE_SCATTER);
-            k_scatter<<<nblk(n, 256), 256, 0, st>>>(d_points, g, p->keys_in, p->vals_in, p->bucket_begin,
+            k_scatter<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(nblk((n + 3) / 4, 256), (int64_t)p->num_sms * 16)),
+                        256, 0, st>>>(d_points, g, p->keys_in, p->vals_in, p->bucket_begin,
                                                      (uint32_t)p->nbuckets, n, p->rec_sorted, p->d_bw,
                                                      p->bw_sorted);
         }
