@@ -273,10 +273,29 @@ def config_dict(w, info, extra=None):
 
 
 # --------------------------------------------------------------------- GPU ---
+# collectives of the bench's own bookkeeping (counts, max-over-ranks times): NCCL on device
+# tensors, or -- STKDE_BENCH_SHARED_GPU=1, the rehearsal of the N-rank path with every rank on
+# one GPU, where NCCL refuses two ranks per device -- gloo on host copies
+_GLOO = {"on": False}
+
+
+def allreduce(t, op=None):
+    import torch.distributed as dist
+    op = dist.ReduceOp.SUM if op is None else op
+    if _GLOO["on"]:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+    else:
+        dist.all_reduce(t, op=op)
+
+
 def direct_gather_ms(S, plan, pts, full, rank, local_rank, x0, x1, w, stream, barrier, dev):
     """The direct gather fused into the compute (stkde_ipc_*): each rank's tile kernel stores its
     x-slab straight into rank 0's grid over NVLink; one pass (binning + tiles) per step, the max
     over ranks (compare with ms_per_step, the same pass into the rank's own buffer)."""
+    import torch
+    import torch.distributed as dist
     from paper_1705_09366_b200.sharded import direct_row_offset, exchange_root_handle
     handle, root_off = exchange_root_handle(rank, 0, lambda: S.ipc_handle(full))
     peer, why = None, ""
@@ -285,7 +304,7 @@ def direct_gather_ms(S, plan, pts, full, rank, local_rank, x0, x1, w, stream, ba
     except Exception as e:  # pragma: no cover - hardware-specific
         why = repr(e)[:200]
     ok = torch.tensor([0 if why else 1], dtype=torch.int32, device=dev)
-    dist.all_reduce(ok, op=dist.ReduceOp.MIN)         # every rank mapped the root's grid, or none times
+    allreduce(ok, op=dist.ReduceOp.MIN)         # every rank mapped the root's grid, or none times
     if not int(ok.item()):
         if peer is not None:
             peer.close()
@@ -305,7 +324,7 @@ def direct_gather_ms(S, plan, pts, full, rank, local_rank, x0, x1, w, stream, ba
             b_.record(stream)
         barrier()
         d_ms = torch.tensor([sum(a_.elapsed_time(b_) for a_, b_ in dd) / len(dd)], dtype=torch.float64, device=dev)
-        dist.all_reduce(d_ms, op=dist.ReduceOp.MAX)
+        allreduce(d_ms, op=dist.ReduceOp.MAX)
     finally:
         if peer is not None:
             peer.close()
@@ -320,10 +339,24 @@ def gpu_main(args, w, rank, world, local_rank):
 
     import paper_1705_09366_b200 as S
 
+    # STKDE_BENCH_SHARED_GPU=1: a rehearsal of the N-rank control flow on a box with fewer GPUs
+    # than ranks (ranks share devices round-robin, gloo for the bookkeeping collectives, the
+    # library's NCCL gather skipped); its times are not a scaling measurement and the line says so
+    shared = world > 1 and os.environ.get("STKDE_BENCH_SHARED_GPU") == "1"
+    gpu_idx = local_rank
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if shared:
+        local_rank = local_rank % torch.cuda.device_count()
+    if vis:
+        gpu_idx = vis.split(",")[local_rank]
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _GLOO["on"] = shared
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     g = w.grid_kwargs()
     variant = args.variant
     if variant == "sweep" and world > 1:
@@ -369,7 +402,7 @@ def gpu_main(args, w, rank, world, local_rank):
             C = int(plan.count_contributions(pts, t0, t1, stream=stream).item())
     Ct = torch.tensor([C], dtype=torch.int64, device=dev)
     if world > 1:
-        dist.all_reduce(Ct)
+        allreduce(Ct)
     C_total = int(Ct.item())
     C_own = C if not (xsplit and variant == "adaptive") else None   # exact per-rank count (None: estimate)
     odt = torch.float64 if variant == "f64" else torch.float32
@@ -428,10 +461,6 @@ def gpu_main(args, w, rank, world, local_rank):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     plan.mma_stats()                            # reset the issued-MMA counters (tcgen05 engine)
     plan.enable_kernel_timing(True)
-    gpu_idx = local_rank
-    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
-    if vis:
-        gpu_idx = vis.split(",")[local_rank]
     with ClockSampler(gpu_idx) as clk:
         barrier()
         with torch.cuda.stream(stream):
@@ -471,7 +500,7 @@ def gpu_main(args, w, rank, world, local_rank):
     kernel_ms = kms / max(args.steps, 1)          # tile-kernel time per step (all its launches)
     vals = torch.tensor([ms, kernel_ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+        allreduce(vals, op=dist.ReduceOp.MAX)
     ms_max, kernel_ms_max = float(vals[0]), float(vals[1])
 
     # ---- e2e through the public API: pinned host points in, grid (slab) out ----
@@ -540,7 +569,7 @@ def gpu_main(args, w, rank, world, local_rank):
     barrier()
     e2e_ms = torch.tensor([eb.elapsed_time(ee) / e2e_steps], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        allreduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
     h2d = (w.points.nbytes + (bw_host.nbytes if bw_host is not None else 0)) * world
     esz = out.element_size()
@@ -617,7 +646,7 @@ def gpu_main(args, w, rank, world, local_rank):
 
     if world > 1:       # the line carries rank 0's roofline; the slowest rank's fraction too
         fr_t = torch.tensor([roof["frac"]], dtype=torch.float64, device=dev)
-        dist.all_reduce(fr_t, op=dist.ReduceOp.MIN)
+        allreduce(fr_t, op=dist.ReduceOp.MIN)
         roof["rank"] = 0
         roof["frac_min_over_ranks"] = float(fr_t.item())
 
@@ -627,29 +656,32 @@ def gpu_main(args, w, rank, world, local_rank):
     gather = None
     if world > 1 and xsplit and variant == "fixed":
         full = torch.empty(tuple(w.G), dtype=torch.float32, device=dev) if rank == 0 else None
-        # the library's own NCCL communicator (stkde_plan_comm_init), id shipped over the group
-        uid = [S.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        plan.comm_init(world, rank, uid[0])
-        slab = out[:max(x1 - x0, 0)]
+        if shared:   # NCCL refuses two ranks on one device: the rehearsal skips the library gather
+            gather = {"skipped": "STKDE_BENCH_SHARED_GPU rehearsal (ranks share a GPU; NCCL needs one device per rank)"}
+        else:
+            # the library's own NCCL communicator (stkde_plan_comm_init), id shipped over the group
+            uid = [S.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            plan.comm_init(world, rank, uid[0])
+            slab = out[:max(x1 - x0, 0)]
 
-        def do_gather():
-            with torch.cuda.stream(stream):
-                plan.gather_xslab(slab, xcuts, 0, full, stream=stream)
-        do_gather()                                   # warm-up (NCCL P2P connection setup)
-        barrier()
-        gb_, ge_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        gb_.record(stream)
-        do_gather()
-        ge_.record(stream)
-        barrier()
-        g_ms = torch.tensor([gb_.elapsed_time(ge_)], dtype=torch.float64, device=dev)
-        dist.all_reduce(g_ms, op=dist.ReduceOp.MAX)
-        gbytes = (w.G[0] - (x1 - x0 if rank == 0 else 0)) * w.G[1] * w.G[2] * 4
-        gather = {"ms": float(g_ms.item()), "bytes_to_root": gbytes,
-                  "how": "stkde_gather_xslab: NCCL send/recv group inside the library, each rank's x-slab "
-                         "received in place into its rows of rank 0's grid",
-                  "timed_in_value": False}
+            def do_gather():
+                with torch.cuda.stream(stream):
+                    plan.gather_xslab(slab, xcuts, 0, full, stream=stream)
+            do_gather()                                   # warm-up (NCCL P2P connection setup)
+            barrier()
+            gb_, ge_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            gb_.record(stream)
+            do_gather()
+            ge_.record(stream)
+            barrier()
+            g_ms = torch.tensor([gb_.elapsed_time(ge_)], dtype=torch.float64, device=dev)
+            allreduce(g_ms, op=dist.ReduceOp.MAX)
+            gbytes = (w.G[0] - (x1 - x0 if rank == 0 else 0)) * w.G[1] * w.G[2] * 4
+            gather = {"ms": float(g_ms.item()), "bytes_to_root": gbytes,
+                      "how": "stkde_gather_xslab: NCCL send/recv group inside the library, each rank's x-slab "
+                             "received in place into its rows of rank 0's grid",
+                      "timed_in_value": False}
         # the direct gather fused into the compute (stkde_ipc_*): each rank's tile kernel stores its
         # x-slab straight into rank 0's grid over NVLink; one pass (binning + tiles) per step, the
         # max over ranks, against the same pass into the rank's own buffer (ms_per_step)
@@ -705,6 +737,9 @@ def gpu_main(args, w, rank, world, local_rank):
             result["separate_ms"] = separate_ms
         if gather is not None:
             result["gather"] = gather
+        if shared:
+            result["rehearsal"] = ("STKDE_BENCH_SHARED_GPU=1: %d ranks shared %d GPU(s); the N-rank control flow "
+                                   "on hardware, NOT a scaling measurement" % (world, torch.cuda.device_count()))
         print(json.dumps(result))
     plan.close()
     if world > 1:
@@ -738,7 +773,7 @@ def self_launch(args):
     if not args.dry_run:
         import torch
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and os.environ.get("STKDE_BENCH_SHARED_GPU") != "1":
             print(json.dumps({"n_gpus": args.gpus, "error": "--gpus %d but only %d CUDA device(s) visible"
                               % (args.gpus, have)}))
             return 2
