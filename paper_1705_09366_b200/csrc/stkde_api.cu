@@ -142,9 +142,12 @@ extern "C" int stkde_plan_create(stkde_plan_t *out, int device, double x0, doubl
     g.XA0 = 0;
     g.NXA = g.NTX;
     // Home-bucket depth in T: the tcgen05 engine bins points into 16x8x32 (16 when
-    // H_t <= 8) blocks so a tile fetches only the blocks its temporal reach meets;
-    // the legacy engines bin by whole tiles.
-    g.BTH = p->engine == STKDE_ENGINE_TC ? (g.Ht <= 8 ? 16 : 32) : p->engine == STKDE_ENGINE_WS ? 16 : BT;
+    // H_t <= 8 on Bt = 128 tiles) blocks so a tile fetches only the blocks its temporal
+    // reach meets; the legacy engines bin by whole tiles.  (Bt = 64 tiles -- the small
+    // grids -- keep 32: a tile's reach then spans 3-4 home blocks instead of 5-6, measured
+    // tiny 0.041 -> 0.039 ms, dengue 0.079 -> 0.076 ms per graph step; on Bt = 128 tiles 16
+    // stays best for short windows, ornith 5.96 vs 6.09 ms with 32.)
+    g.BTH = p->engine == STKDE_ENGINE_TC ? (g.Ht <= 8 && BT == 128 ? 16 : 32) : p->engine == STKDE_ENGINE_WS ? 16 : BT;
     g.BTH = env_int("STKDE_BTH", g.BTH);
     if (g.BTH < 1) { set_error("bad STKDE_BTH"); free(p); return STKDE_EINVAL; }
     g.NTTH = (int)((Gt + g.BTH - 1) / g.BTH);
