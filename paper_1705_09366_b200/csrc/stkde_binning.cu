@@ -330,6 +330,10 @@ __device__ __forceinline__ uint32_t tile_candidates(const GridParams &g, const u
     return s;
 }
 
+// 8-bit log-class work-list keys (one radix pass; 0: exact 16-bit counts, two passes)
+#ifndef STKDE_WL_KEY8
+#define STKDE_WL_KEY8 1
+#endif
 // K3a: per slab tile, candidate count and work-list sort key (stable radix sort, ascending).
 //   order 0 (LPT, "most loaded subdomain first"): descending count;
 //   order 1 (locality): tiles with >= `heavy` candidates first by descending count, then the
@@ -345,9 +349,20 @@ __global__ void k_tile_counts(GridParams g, const uint32_t *__restrict__ bucket_
     if (ls >= nsl) return;
     int a = ls % g.NXA + g.XA0, b = (ls / g.NXA) % g.NTY, c = ls / (g.NXA * g.NTY) + c0;
     uint32_t cnt = tile_candidates(g, bucket_begin, a, b, c);
+#if STKDE_WL_KEY8
+    // 8-bit keys (one radix pass): the count's log class 16 log2(cnt + 1) from its leading bit
+    // and the next four (steps of <= 6.25 %, monotone; capped at 254), descending; locality
+    // order: the non-heavy tiles share key 255 and keep their slab-tile order (stable sort)
+    const uint32_t v = cnt + 1u;
+    const int e = 31 - __clz(v);
+    const uint32_t frac = (e >= 4 ? v >> (e - 4) : v << (4 - e)) & 15u;
+    const uint32_t cls = min(16u * (uint32_t)e + frac, 254u);
+    lkey[ls] = (order == 0 || cnt >= heavy) ? 254u - cls : 255u;
+#else
     // locality order in 16-bit keys: the non-heavy tiles share the largest key, and the stable
     // sort keeps them in slab-tile order (two radix passes instead of three)
     lkey[ls] = order == 0 ? 0xFFFFu - min(cnt, 0xFFFFu) : (cnt >= heavy ? 0xFFFEu - min(cnt, 0xFFFEu) : 0xFFFFu);
+#endif
     lval[ls] = (uint32_t)ls;
     tcnt[ls] = cnt;
 }
@@ -626,7 +641,7 @@ int launch_worklist(stkde_plan_s *p, int c0, int c1, cudaStream_t st) {
     int nsl = g.NXA * g.NTY * (c1 - c0);
     // locality order only for grids with many tiles per SM (few tiles: LPT balances the SMs)
     const int order = p->order >= 0 ? p->order : (nsl >= 64 * p->num_sms ? 1 : 0);
-    const int kbits = 16;                            // LPT and locality keys < 2^16 (k_tile_counts)
+    const int kbits = STKDE_WL_KEY8 ? 8 : 16;        // LPT and locality keys (k_tile_counts)
     if (nsl <= WL_CAP && p->wl_small) {              // small slab: the whole work list in one CTA
         k_worklist_small<<<1, WL_THR, 0, st>>>(g, p->bucket_begin, c0, nsl, order, (uint32_t)p->heavy, p->chunk,
                                                p->tile_cnt, p->lpt_val_out, p->chunk_off, p->items, p->max_items,
