@@ -186,13 +186,13 @@ int stkde_count_contributions_box(stkde_plan_t plan, const float *d_points, int6
  * overwrite, asynchrony, determinism and slab rules as stkde_compute /
  * stkde_compute_slab.  Needs the tcgen05 engine (H_s <= 120); otherwise
  * STKDE_EINVAL.
- * Accuracy: the fixed-point factors are scaled by the largest per-point weight
- * max_i 1/(hs_i^2 ht_i); each contribution carries <= 8.3e-7 of that full scale.
- * The result is within 1e-5 of the grid's maximum whenever every hs_i >= sres and
- * ht_i >= tres; with sub-voxel per-point bandwidths the heaviest points may cover
- * no voxel centre and a maximum built from many far smaller contributions can
- * deviate more (up to 1.9e-4 of the maximum observed, tests/test_gpu_fuzz.py;
- * DESIGN.md section 5).  stkde_compute_adaptive_slab_f64 has no such scale. */
+ * Accuracy: the fixed-point factors are scaled by max_i W_i s_i, W_i = 1/(hs_i^2 ht_i)
+ * and s_i the point's spatial factor at its nearest voxel centre; each contribution
+ * carries <= 8.3e-7 of that full scale.  The result is within 1e-5 of the grid's
+ * maximum whenever every hs_i >= sres and ht_i >= tres; with sub-voxel per-point
+ * bandwidths a maximum built from hundreds of far smaller contributions can deviate
+ * more (up to 3.8e-5 of the maximum observed, tests/test_gpu_fuzz.py; DESIGN.md
+ * section 5).  stkde_compute_adaptive_slab_f64 has no such scale. */
 int stkde_compute_adaptive(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
                            float *d_grid, void *stream);
 int stkde_compute_adaptive_slab(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,

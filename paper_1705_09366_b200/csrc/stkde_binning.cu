@@ -74,17 +74,36 @@ __device__ __forceinline__ uint32_t prep_point(const float *__restrict__ pts, in
     PointRec r;
     uint32_t key = sentinel;
     bool bw_ok = true;
+    PointBw b{0.f, 0.f, 0.f, 0.f};
     if (bw) {
-        PointBw b{0.f, 0.f, 0.f, 0.f};
         bw_ok = make_bw(g, bw, i, &b);
         if (!bw_ok) atomicOr(err, 4);
-        else {
-            const double ws = g.sres / (double)b.hs, wt = g.tres / (double)b.ht;
-            atomicMax(wmax, __float_as_uint((float)(ws * ws * wt)));
-        }
         if (bw_rec) bw_rec[i] = b;
     }
-    if (!make_rec(g, x, y, t, &r)) {
+    const bool rec_ok = make_rec(g, x, y, t, &r);
+    if (bw && bw_ok && rec_ok) {
+        // The fixed-point full scale of an adaptive call: max_i W_i s_i, s_i >= the point's largest
+        // spatial factor over ALL voxel columns -- reached at the column nearest to it in x and in y
+        // (k_s decreases in |u| and |v| separately).  A point whose disc holds no
+        // voxel centre near its peak (sub-voxel hs_i) then no longer inflates the scale (DESIGN.md
+        // section 5, "small contributions").  eps covers the FP32 rounding of the generators'
+        // tile-relative position (|b_x| < 256: half an ulp <= 2^-17) times sres/hs_i, the 1.0001
+        // their FP32 products and this value's own rounding, so W_i/scale * a_x * a_y <= 1 holds
+        // for every column in the tile kernel's arithmetic.  Depends on the points only: every
+        // slab of a grid sees the same scale (slabs stay bitwise equal to the full grid).
+        const double ws = g.sres / (double)b.hs, wt = g.tres / (double)b.ht;
+        const double is = (double)b.inv_rs, eps = is * 1.52587890625e-05 + 1e-6;
+        const double ux = fabs(0.5 - (double)r.fx) * is, uy = fabs(0.5 - (double)r.fy) * is;
+        double sp;
+        if (g.kernel == STKDE_KERNEL_PRINTED) {
+            const double ax = fmin(fmax(1.0 - ux, 0.0) + eps, 1.0), ay = fmin(fmax(1.0 - uy, 0.0) + eps, 1.0);
+            sp = ax * ax * ay * ay;
+        } else {
+            sp = fmin(fmax(1.0 - ux * ux - uy * uy, 0.0) + 4.0 * eps, 1.0);
+        }
+        atomicMax(wmax, __float_as_uint((float)(ws * ws * wt * sp * 1.0001)));
+    }
+    if (!rec_ok) {
         atomicOr(err, 1);
     } else if (bw_ok && reaches_grid(g, r) && r.T + g.Ht >= t_begin && r.T - g.Ht < t_end &&
                r.X + g.Hs >= g.XA0 * BX && r.X - g.Hs < (g.XA0 + g.NXA) * BX) {
