@@ -257,3 +257,43 @@ def test_random_plan_f64_parity(S, oracle_mod, k):
         refa = oracle_mod.stkde_pb_adaptive(pts, bw, kernel=kernel, **g)
         gpua = run_f64(S, pts, kernel=kernel, bw=bw, **g)
         assert_f64_parity(gpua, refa.vol, len(pts), what="f64 adaptive fuzz %d %s kernel %d" % (k, g, kernel))
+
+
+@pytest.mark.parametrize("kernel", [0, 1], ids=["printed", "classical"])
+def test_adaptive_scale_never_overflows(S, oracle_mod, kernel):
+    # The adaptive full scale is max_i W_i s_i with s_i the point's spatial factor at its nearest
+    # voxel column (k_prep): a point whose nearest centre sits just inside its disc edge makes s_i
+    # tiny, and W_i / scale * a_x * a_y must still not exceed 1 in the generators' FP32 arithmetic
+    # (a fixed-point code above 2^23 - 1 would wrap).  One point per call (it alone sets the
+    # scale), u = d / hs_i from 0.5 to 0.99999 at its nearest centre, at tile-relative positions
+    # up to 16 + H_s with the plan's H_s = 100; a wrapped code would miss the oracle grossly.
+    g = dict(x0=0.0, y0=0.0, t0=0.0, sres=1.0, tres=1.0, Gx=260, Gy=40, Gt=12, hs=100.0, ht=2.0)
+    r = synth.SplitMix64(777 + kernel)
+    dev = torch.device("cuda", 0)
+    worst = 0.0
+    with S.Plan(max_n=1, kernel=kernel, device=0, **g) as p:
+        for j, u in enumerate([0.5, 0.9, 0.99, 0.999, 0.9999, 0.99999] * 4):
+            v = r.uniform01(6)
+            X = [0, 15, 16, 127, 143, 259][int(v[0] * 6) % 6]
+            Y = int(v[1] * g["Gy"])
+            fx, fy = 0.02 + 0.96 * v[2], 0.02 + 0.96 * v[3]
+            # distance to the nearest centre in the axis the kernel's factor is evaluated on
+            d = max(abs(fx - 0.5), abs(fy - 0.5)) if kernel == 0 else float(np.hypot(fx - 0.5, fy - 0.5))
+            hs_i = np.float32(min(max(d / u, 1e-3), 100.0))
+            pts = np.array([[X + fx, Y + fy, 5.0 + v[4]]], np.float32)
+            bw = np.array([[hs_i, np.float32(0.8 + v[5])]], np.float32)
+            ref = oracle_mod.stkde_pb_adaptive(pts, bw, kernel=kernel, **g)
+            gpu = p.compute_adaptive(torch.from_numpy(pts).to(dev), torch.from_numpy(bw).to(dev)).cpu().numpy()
+            p.check()
+            clear = ref.amb == 0
+            assert np.array_equal((gpu > 0) & clear, (ref.vol > 0) & clear), (j, u, pts, bw)
+            if ref.vol.max() > 0:
+                # gross-error check: a wrapped code is off by the full scale, i.e. O(1) of this grid's
+                # maximum.  Not the 1e-5 parity bound: at u -> 1 the grid's maximum is (1 - u)^2 or
+                # 1 - u^2 ~ 1e-5 of the point's peak, where the FP32 in-voxel fraction alone (2^-24 of
+                # a voxel) moves the value by ~1e-3 of itself (measured: 1.8e-3 at
+                # u = 0.99999, classical kernel).  The achieved figure is printed.
+                e = float((np.abs(gpu - ref.vol) - ref.slack).max() / ref.vol.max())
+                worst = max(worst, e)
+                assert e <= (1e-5 if u <= 0.99 else 2e-2), (j, u, pts.tolist(), bw.tolist(), e)
+    print("adaptive single points near the disc edge: worst |gpu - oracle| / max = %.2e" % worst)
