@@ -191,8 +191,8 @@ int stkde_count_contributions_box(stkde_plan_t plan, const float *d_points, int6
  * carries <= 8.3e-7 of that full scale.  The result is within 1e-5 of the grid's
  * maximum whenever every hs_i >= sres and ht_i >= tres; with sub-voxel per-point
  * bandwidths a maximum built from hundreds of far smaller contributions can deviate
- * more (up to 3.8e-5 of the maximum observed, tests/test_gpu_fuzz.py; DESIGN.md
- * section 5).  stkde_compute_adaptive_slab_f64 has no such scale. */
+ * more (up to 1.5e-4 of the maximum over 1500 random draws, tests/test_gpu_fuzz.py;
+ * DESIGN.md section 5).  stkde_compute_adaptive_slab_f64 has no such scale. */
 int stkde_compute_adaptive(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
                            float *d_grid, void *stream);
 int stkde_compute_adaptive_slab(stkde_plan_t plan, const float *d_points, const float *d_bw, int64_t n,
