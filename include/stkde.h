@@ -37,6 +37,17 @@
  *     short-window FP32 engine (WS) for any boundary (every voxel sums in
  *     candidate order), with the other FP32 engines for time-slab boundaries
  *     that are multiples of the tile height Bt.
+ *   - Accuracy (float32 grids): |result - definition| <= 1e-5 of the grid's
+ *     maximum and an exact support mask (value > 0), guaranteed where every
+ *     bandwidth spans at least one voxel (hs >= sres, ht >= tres).  With a
+ *     disc or window narrower than one voxel the maximum can lie far below one
+ *     point's peak -- the scale of the fixed-point / FP32 factors -- and the
+ *     bound can be missed (up to 1.9e-4 of the maximum over 1500 random
+ *     plans; support still exact).  The temporal gate is decided in FP32: a
+ *     pair within ~8e-6 (relative) of the window edge may be gated the other
+ *     way, which changes a value by < 4e-6 of the maximum (K_t is zero at the
+ *     edge) but can flip the support bit of such a voxel.  The float64 calls
+ *     (stkde_compute_f64 ...) have neither limit.  DESIGN.md sections 5, 3.10.
  *   - Return codes: STKDE_OK (0) or a negative STKDE_E* value; the message
  *     of the most recent error on the calling thread is stkde_last_error().
  */
